@@ -1,0 +1,188 @@
+// ldpc_common.cuh -- shared device types and arithmetic for the sm_100a decoder.
+//
+// Arithmetic follows the reference engine's operation order exactly
+// (/root/reference/pkg/src/ldpc_ids/_engine.py, "E:<line>"): ordered tanh
+// products, clip to +-(1-1e-12) before atanh, +-30 clamps, the stable logistic.
+// Compiled with -fmad=false so no multiply-add is contracted into an FMA that
+// the float64 reference would round twice.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ldpc {
+
+constexpr int kCounters = 8;
+enum Counter { C_PROP = 0, C_V2C, C_PRE, C_CI, C_CMP, C_MSEL, C_KHITS, C_KTRIALS };  // E:17-25
+enum Kernel { KERNEL_EXACT = 0, KERNEL_MINSUM = 1 };                                // E:27-28
+enum Kind {
+  KIND_FLOODING = 0, KIND_RBP = 1, KIND_CIRBP = 2, KIND_LMDRBP = 3, KIND_SLMDRBP = 4,
+  KIND_LMD_CIRBP = 5, KIND_ME_CIRBP = 6, KIND_ME_LMD_CIRBP = 7, KIND_LAYERED = 8, KIND_ME_RBP = 9
+};
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxTreeLevels = 6;  // 32-ary: 32^6 > 1e9 leaves
+
+// Immutable device-side Tanner graph (edge ids in (check, vn) order, codes.py:251-275).
+struct DevGraph {
+  int N, M, E;
+  int max_dv, max_dc, max_items;  // max_items = max two-hop set size
+  const int* edge_cn;   // [E]
+  const int* edge_vn;   // [E]
+  const int* cn_ptr;    // [M+1]
+  const int* vn_ptr;    // [N+1]
+  const int* vn_edges;  // [E]
+  // layered schedule: checks grouped in dependency levels (same result as m = 0..M-1 in order)
+  int n_levels;
+  const int* level_ptr;     // [n_levels+1]
+  const int* level_checks;  // [M]
+};
+
+// 32-ary max-tree geometry over `n` leaves (levels 1..L; level L has <= 32 nodes).
+struct TreeGeom {
+  int levels;                      // number of internal levels (>= 1)
+  int size[kMaxTreeLevels + 1];    // size[0] = leaves
+  int off[kMaxTreeLevels + 1];     // node offset of level l (l >= 1) inside the key array
+  int total;                       // total internal nodes
+};
+
+inline TreeGeom make_tree(int n) {
+  TreeGeom t{};
+  t.size[0] = n;
+  int l = 0, tot = 0;
+  do {
+    int s = (t.size[l] + 31) / 32;
+    ++l;
+    t.size[l] = s;
+    t.off[l] = tot;
+    tot += s;
+  } while (t.size[l] > 32 && l < kMaxTreeLevels);
+  t.levels = l;
+  t.total = tot;
+  return t;
+}
+
+// ------------------------------------------------------------------ math
+
+template <typename T> struct Num;
+template <> struct Num<double> {
+  using Key = unsigned long long;
+  static constexpr double kLlrMax = 30.0;            // E:13
+  static constexpr double kAtanhClip = 1.0 - 1e-12;  // E:14
+  static constexpr double kBig = 1e300;              // E:68
+  __device__ static double tanh_(double x) { return tanh(x); }
+  __device__ static double atanh_(double x) { return atanh(x); }
+  __device__ static double exp_(double x) { return exp(x); }
+  __device__ static double abs_(double x) { return fabs(x); }
+  // order-preserving key for values >= +0; 0 is reserved for padding / excluded
+  __device__ static Key key(double v) {
+    return v >= 0.0 ? (Key)__double_as_longlong(v) + 1ull : 0ull;
+  }
+};
+template <> struct Num<float> {
+  using Key = unsigned int;
+  static constexpr float kLlrMax = 30.0f;
+  static constexpr float kAtanhClip = (float)(1.0 - 1e-12);  // rounds to 1.0f: fp32 saturates earlier
+  static constexpr float kBig = 3.0e38f;
+  __device__ static float tanh_(float x) { return tanhf(x); }
+  __device__ static float atanh_(float x) { return atanhf(x); }
+  __device__ static float exp_(float x) { return expf(x); }
+  __device__ static float abs_(float x) { return fabsf(x); }
+  __device__ static Key key(float v) { return v >= 0.0f ? __float_as_uint(v) + 1u : 0u; }
+};
+
+template <typename T> __device__ __forceinline__ T clampv(T x) {  // E:31-37
+  if (x > Num<T>::kLlrMax) return Num<T>::kLlrMax;
+  if (x < -Num<T>::kLlrMax) return -Num<T>::kLlrMax;
+  return x;
+}
+
+template <typename T> __device__ __forceinline__ T p0(T llr) {  // E:40-46
+  if (llr >= T(0)) return T(1) / (T(1) + Num<T>::exp_(-llr));
+  T e = Num<T>::exp_(llr);
+  return e / (T(1) + e);
+}
+
+template <typename T> __device__ __forceinline__ T ci_of(T tot, T pre_tot) {
+  return Num<T>::abs_(p0(tot) - p0(pre_tot));
+}
+
+// Product -> C2V (E:62-66 / E:99-103).
+template <typename T> __device__ __forceinline__ T atanh_msg(T prod, int count) {
+  if (count == 0) return T(0);
+  if (prod > Num<T>::kAtanhClip) prod = Num<T>::kAtanhClip;
+  else if (prod < -Num<T>::kAtanhClip) prod = -Num<T>::kAtanhClip;
+  return clampv(T(2) * Num<T>::atanh_(prod));
+}
+
+// C2V of check [a, b) excluding edge `skip` from cached inputs `in`:
+// exact kernel: in = tanh(v2c/2) (E:85-103); min-sum: in = v2c (E:67-82).
+template <typename T, int KERNEL>
+__device__ __forceinline__ T cn_msg_cached(const T* in, int a, int b, int skip) {
+  if (KERNEL == KERNEL_EXACT) {
+    T prod = T(1);
+    for (int e = a; e < b; ++e)
+      if (e != skip) prod *= in[e];
+    return atanh_msg(prod, b - a - ((skip >= a && skip < b) ? 1 : 0));
+  } else {
+    T sign = T(1), mag = Num<T>::kBig;
+    int count = 0;
+    for (int e = a; e < b; ++e) {
+      if (e == skip) continue;
+      T v = clampv(in[e]);
+      if (v < T(0)) { sign = -sign; v = -v; }
+      if (v < mag) mag = v;
+      ++count;
+    }
+    if (count == 0) return T(0);
+    return clampv(sign * mag);
+  }
+}
+
+// ------------------------------------------------------------ warp helpers
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp max of keys (REDUX) -> lowest lane holding it.  Returns (key, lane).
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k, int* lane_out) {
+  unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  unsigned mh = __reduce_max_sync(kFull, hi);
+  unsigned lo_c = (hi == mh) ? lo : 0u;
+  unsigned ml = __reduce_max_sync(kFull, lo_c);
+  unsigned bal = __ballot_sync(kFull, hi == mh && lo == ml);
+  *lane_out = __ffs(bal) - 1;
+  return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned warp_max_key(unsigned k, int* lane_out) {
+  unsigned m = __reduce_max_sync(kFull, k);
+  *lane_out = __ffs(__ballot_sync(kFull, k == m)) - 1;
+  return m;
+}
+
+// Max key with the smallest companion index among ties (index < 2^31).
+template <typename K>
+__device__ __forceinline__ K warp_max_key_minidx(K k, int idx, int* idx_out) {
+  int ln;
+  K m = warp_max_key(k, &ln);
+  unsigned cand = (k == m) ? (unsigned)idx : 0xffffffffu;
+  *idx_out = (int)__reduce_min_sync(kFull, cand);
+  return m;
+}
+
+__device__ __forceinline__ int warp_sum(int v) { return (int)__reduce_add_sync(kFull, (unsigned)v); }
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  int lane = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int t = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+
+}  // namespace ldpc
