@@ -1,0 +1,364 @@
+"""Benchmark: decoded frames/s and C2V edge updates/s per schedule (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (default): BASELINE.json configs[1] -- the WiFi-shaped n=648 QC code
+(Z=27), BPSK-AWGN at Eb/N0 = 2.0 dB (mid-sweep), i_max = 3, batch 100,000
+frames, and every schedule the config names (flooding, layered, RBP, CIRBP,
+LMDRBP, sLMDRBP, LMD-CIRBP, ME-CIRBP M=4, ME-RBP M=4).  One step = the batch
+decoded once by every schedule.  value = total C2V edge updates / time over
+the K timed steps (whole job, all ranks).  The batch's LLRs (259 MB) exceed
+the 126 MB L2, so every step streams its inputs from HBM.
+
+--impl reference: the reference's decode algorithm on the host cores (the C
+oracle port, oracle/ldpc_oracle.c, all threads), same config/metric, each step
+a bounded seeded sample of the batch.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (config key, ebn0, i_max, batch, [(kind, n_p)])
+    "C1": ("C1", 2.0, 3, 100_000,
+           [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1), ("lmdrbp", 1), ("slmdrbp", 1),
+            ("lmd_cirbp", 1), ("me_cirbp", 4), ("me_rbp", 4)]),
+    "C0": ("C0", 2.0, 5, 10_000, [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1)]),
+    "C2": ("C2", 1.0, 3, 100_000, [("layered", 1), ("rbp", 1), ("cirbp", 1), ("me_cirbp", 1),
+                                   ("me_cirbp", 4), ("me_cirbp", 16)]),
+    "C3": ("C3", 1.0, 10, 10_000, [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1),
+                                   ("me_cirbp", 64)]),
+}
+
+CI_KINDS = {"cirbp", "lmd_cirbp", "me_cirbp", "me_lmd_cirbp"}
+
+
+def bytes_per_update(kind, counters, E, N, elem):
+    """Algorithmic message-state bytes per C2V update,
+    in units of the state element size `elem` (4 = fp32 figures, 8 = fp64)."""
+    s = elem / 4.0
+    P = max(1, int(counters[:, 0].sum()))
+    if kind == "flooding":
+        return s * (16 + 8 * N / E)
+    if kind == "layered":
+        return s * 16
+    V, R, I = (int(counters[:, k].sum()) for k in (1, 2, 3))
+    base = 20 + (8 if kind in CI_KINDS else 0)
+    return s * (base + (12 * V + 28 * R + 8 * I) / P)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() and args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available() and args.impl == "ours":
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def make_inputs(spec, ebn0, start, count):
+    from paper_2102_11089_b200.channel import llr_batch
+    return llr_batch(spec, ebn0, seed=0, start=start, count=count, dtype=np.float32)
+
+
+def run_reference(args, wl):
+    """Reference algorithm (oracle port) on all host cores; rank 0 only."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from oracle import pyoracle
+    from paper_2102_11089_b200 import configs
+    from paper_2102_11089_b200.codes import build_tanner
+    key, ebn0, i_max, batch, scheds = wl
+    spec = getattr(configs, f"make_{key.lower()}_code")()
+    g = build_tanner(spec.h)
+    cores = os.cpu_count() or 1
+    sample = args.ref_sample or max(64, min(4096, 2 * cores * 64))
+    llr = make_inputs(spec, ebn0, 0, sample).astype(np.float64)
+    def step():
+        upd = frames = 0
+        t0 = time.perf_counter()
+        for kind, n_p in scheds:
+            r = pyoracle.decode_batch(g, llr, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
+                                      threads=cores)
+            upd += int(r["prop"].sum())
+            frames += len(llr)
+        return upd, frames, time.perf_counter() - t0
+    for _ in range(args.warmup):
+        step()
+    tot_u = tot_f = tot_t = 0
+    for _ in range(args.steps):
+        u, f, t = step()
+        tot_u += u
+        tot_f += f
+        tot_t += t
+    val = tot_u / tot_t
+    line = {
+        "impl": "reference", "metric": "C2V edge updates/s (all C1 schedules); decoded frames/s",
+        "value": val, "unit": "C2V edge updates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "frames_per_s": tot_f / tot_t,
+        "config": {"workload": f"{key}: " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+                   "code": spec.label, "ebn0_db": ebn0, "i_max": i_max, "batch": sample},
+        "cpu_baseline": {"value": val, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
+                         "sample": f"first {sample} frames of the seeded batch, every schedule"},
+        "e2e": {"value": val, "unit": "C2V edge updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
+    """Oracle on a bounded sample, all host cores (rank 0, N=1 only)."""
+    from oracle import pyoracle
+    key, ebn0, i_max, batch, scheds = wl
+    cores = os.cpu_count() or 1
+    # size the sample from a quick probe so the whole baseline takes ~budget_s
+    probe = llr_host[:cores * 4].astype(np.float64)
+    t0 = time.perf_counter()
+    for kind, n_p in scheds:
+        pyoracle.decode_batch(g, probe, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p, threads=cores)
+    dt = time.perf_counter() - t0
+    n = int(max(cores * 4, min(len(llr_host), len(probe) * budget_s / max(dt, 1e-3))))
+    sample = llr_host[:n].astype(np.float64)
+    per = {}
+    tot_u = 0
+    t0 = time.perf_counter()
+    for kind, n_p in scheds:
+        t1 = time.perf_counter()
+        r = pyoracle.decode_batch(g, sample, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
+                                  threads=cores)
+        u = int(r["prop"].sum())
+        per[f"{kind}" + (f"/M{n_p}" if n_p > 1 else "")] = u / (time.perf_counter() - t1)
+        tot_u += u
+    t = time.perf_counter() - t0
+    return {"value": tot_u / t, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
+            "sample": f"first {n} frames of the batch through every schedule ({t:.1f} s)",
+            "frames_per_s": n * len(scheds) / t, "per_schedule_updates_per_s": per}
+
+
+def run_ours(args, wl):
+    import torch
+    from paper_2102_11089_b200 import configs
+    from paper_2102_11089_b200.codes import build_tanner
+    from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch, device_graph
+
+    rank, world, local = dist_setup(args)
+    key, ebn0, i_max, batch, scheds = wl
+    if args.batch:
+        batch = args.batch
+    spec = getattr(configs, f"make_{key.lower()}_code")()
+    g = build_tanner(spec.h)
+    dg = device_graph(g)
+    E, N = g.n_edges, g.n_vars
+    elem = 8 if args.precision == "f64" else 4
+    dev = torch.device("cuda", torch.cuda.current_device())
+    llr_host = make_inputs(spec, ebn0, rank * batch, batch)
+    llr_pinned = torch.from_numpy(llr_host).pin_memory()
+    llr_dev = llr_pinned.to(dev)
+    cfgs = [ScheduleConfig(kind=k, i_max=i_max, n_p=n_p, precision=args.precision) for k, n_p in scheds]
+    stream = torch.cuda.current_stream(dev)
+    outs = {}
+
+    def one(cfg, idx, src):
+        outs[idx] = decode_batch(g, src, cfg, k_info=spec.k_info, out=outs.get(idx))
+        return outs[idx]["_launches"]
+
+    # warm-up (also yields the per-schedule work, identical every step)
+    for _ in range(max(1, args.warmup)):
+        for i, c in enumerate(cfgs):
+            one(c, i, llr_dev)
+    torch.cuda.synchronize()
+    work = []
+    for i, c in enumerate(cfgs):
+        cnt = outs[i]["counters"].cpu().numpy()
+        fer = float((outs[i]["bit_errors_at"][:, -1] > 0).float().mean().item())
+        work.append({"updates": int(cnt[:, 0].sum()), "bpu": bytes_per_update(c.kind, cnt, E, N, elem),
+                     "fer": fer, "counters": cnt.sum(0)})
+
+    # timed region: device-resident inputs
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in cfgs] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    launches = 0
+    t_start.record(stream)
+    for s in range(args.steps):
+        for i, c in enumerate(cfgs):
+            ev[s][i][0].record(stream)
+            launches += one(c, i, llr_dev)
+            ev[s][i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    sched_ms = [sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps)) / args.steps
+                for i in range(len(cfgs))]
+
+    # e2e: pinned host LLRs in, host results out, through the public API
+    res_host = {i: {k: torch.empty_like(outs[i][k], device="cpu").pin_memory()
+                    for k in ("u_hat", "prop", "converged")} for i in range(len(cfgs))}
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e_start.record(stream)
+    h2d = d2h = 0
+    for s in range(args.steps):
+        src = llr_pinned.to(dev, non_blocking=True)
+        h2d += llr_pinned.numel() * llr_pinned.element_size()
+        for i, c in enumerate(cfgs):
+            one(c, i, src)
+            for k in ("u_hat", "prop", "converged"):
+                res_host[i][k].copy_(outs[i][k], non_blocking=True)
+                d2h += outs[i][k].numel() * outs[i][k].element_size()
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end)
+
+    step_updates = sum(w["updates"] for w in work)
+    t_max = total_ms
+    e_max = e2e_ms
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms, e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max, e_max = tt.tolist()
+    job_updates = step_updates * args.steps * world
+    value = job_updates / (t_max / 1e3)
+    e2e_value = job_updates / (e_max / 1e3)
+
+    # dominant kernel roofline (algorithmic state bytes / kernel time)
+    dom = int(np.argmax(sched_ms))
+    w = work[dom]
+    achieved = w["updates"] * w["bpu"] / (sched_ms[dom] / 1e3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    per = {}
+    for i, (c, wk) in enumerate(zip(cfgs, work)):
+        nm = c.kind + (f"/M{c.n_p}" if c.kind.startswith("me_") else "")
+        per[nm] = {"ms": round(sched_ms[i], 3), "edge_updates_per_s": wk["updates"] / (sched_ms[i] / 1e3),
+                   "frames_per_s": batch / (sched_ms[i] / 1e3), "fer": wk["fer"],
+                   "updates_per_frame": wk["updates"] / batch, "state_bytes_per_update": round(wk["bpu"], 1),
+                   "state_GBps": wk["updates"] * wk["bpu"] / (sched_ms[i] / 1e3) / 1e9}
+    line = {
+        "metric": "C2V edge updates/s (all C1 schedules); decoded frames/s",
+        "value": value, "unit": "C2V edge updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "frames_per_s": batch * len(cfgs) * args.steps * world / (t_max / 1e3),
+        "config": {"workload": f"{key}: " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+                   "code": spec.label, "N": N, "E": E, "ebn0_db": ebn0, "i_max": i_max,
+                   "batch_per_gpu": batch, "l2": "inputs > L2 (batch LLRs %.0f MB)" % (llr_pinned.numel() * 4 / 1e6),
+                   "parallelism": f"frames sharded over {world} GPU(s)"},
+        "per_schedule": per,
+        "roofline": {"bound": "hbm", "kernel": list(per)[dom], "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "note": "algorithmic message-state bytes (SURVEY 8(d) formula, %s) / kernel time; "
+                             "state is SMEM-resident for this code, so HBM peak is the stated "
+                             "denominator of measured" % args.precision},
+        "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, spec, g, llr_host, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C1", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT"):
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,118 @@
+/*
+ * ldpc_b200.h -- C ABI of the B200 dynamic-schedule LDPC decoder.
+ *
+ * Drop-in boundary for the reference's decode path.  The reference binds its
+ * engine from Python as
+ *   _engine._decode_<kind>(edge_cn, edge_vn, cn_ptr, vn_ptr, vn_edges, chl,
+ *                          kernel, i_max, k_info, [gamma | simplified |
+ *                          n_p, n_g, seed], c2v, v2c, pre_c2v, residual,
+ *                          total, pre_total, ci, counters, biterr,
+ *                          biterr_info, trace[, kappa_hits, kappa_trials])
+ *   (/root/reference/pkg/src/ldpc_ids/_engine.py:355-765, argument packing at
+ *    /root/reference/pkg/src/ldpc_ids/schedules.py:82-108, dispatch at
+ *    schedules.py:111-158).
+ * Here the graph arrays become an immutable device-resident handle
+ * (ldpc_graph_create replaces the per-call CSR/CSC arguments, codes.py:251-275),
+ * the per-frame float64 state arrays the caller allocated become a caller-sized
+ * workspace, and one call decodes a whole batch of frames on a CUDA stream.
+ *
+ * All pointers passed to ldpc_decode are DEVICE pointers; ldpc_graph_create
+ * takes HOST arrays.  No call synchronises the stream.  Return value 0 = ok,
+ * negative = error (ldpc_strerror).
+ */
+#ifndef LDPC_B200_H
+#define LDPC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes */
+#define LDPC_OK 0
+#define LDPC_ERR_INVALID (-1)     /* bad argument (mirrors the reference's ValueError) */
+#define LDPC_ERR_UNSUPPORTED (-2) /* graph exceeds a kernel limit (d_v > 32 or d_c > 32) */
+#define LDPC_ERR_CUDA (-3)        /* CUDA runtime error */
+#define LDPC_ERR_WORKSPACE (-4)   /* workspace smaller than ldpc_workspace_size() */
+
+/* schedule kinds: schedules.py:20-21 plus the two fixed/new schedules */
+#define LDPC_FLOODING 0
+#define LDPC_RBP 1
+#define LDPC_CIRBP 2
+#define LDPC_LMDRBP 3
+#define LDPC_SLMDRBP 4
+#define LDPC_LMD_CIRBP 5
+#define LDPC_ME_CIRBP 6
+#define LDPC_ME_LMD_CIRBP 7
+#define LDPC_LAYERED 8
+#define LDPC_ME_RBP 9
+
+/* check-node kernels: kernels.py:20 */
+#define LDPC_KERNEL_EXACT 0
+#define LDPC_KERNEL_MINSUM 1
+
+/* arithmetic of the message state */
+#define LDPC_F64 0 /* reference precision (float64), default */
+#define LDPC_F32 1 /* fast mode */
+
+typedef struct ldpc_graph ldpc_graph_t;
+
+/* ScheduleConfig (schedules.py:24-44) + launch options */
+typedef struct {
+  int32_t kind;           /* LDPC_FLOODING .. LDPC_ME_RBP */
+  int32_t kernel;         /* LDPC_KERNEL_EXACT / LDPC_KERNEL_MINSUM */
+  int32_t i_max;          /* update budget in iterations (i_max * E propagations) */
+  int32_t n_p;            /* multi-edge: VNs (edges for ME-RBP) per round */
+  int32_t n_g;            /* multi-edge: CI quantiser groups */
+  int32_t k_info;         /* info positions for info_bit_errors (n < k_info) */
+  double gamma;           /* CIRBP threshold */
+  int64_t selection_seed; /* multi-edge RNG seed (int64 bit pattern) */
+  int32_t precision;      /* LDPC_F64 / LDPC_F32 */
+  int32_t llr_f64;        /* 0: llr is float32[B][N], 1: float64[B][N] */
+  int32_t max_resident;   /* 0 = auto; else cap on concurrently decoded frames */
+  int32_t force_global;   /* 1 = keep frame state in HBM even if it fits in smem */
+} ldpc_sched_t;
+
+/* Build the device-resident Tanner graph (edge ids in (check, vn) order,
+ * vn_edges = stable argsort of edge_vn).  Replaces build_tanner's arrays
+ * (codes.py:251-275).  Host pointers in; the handle owns device copies. */
+int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int32_t* cn_ptr,
+                      const int32_t* vn_ptr, const int32_t* vn_edges, int32_t N, int32_t M,
+                      int32_t E, ldpc_graph_t** out);
+int ldpc_graph_destroy(ldpc_graph_t* g);
+
+/* graph facts: out[0..6] = N, M, E, max_dv, max_dc, max_two_hop, layered levels */
+int ldpc_graph_info(const ldpc_graph_t* g, int64_t* out7);
+
+/* Bytes of device workspace ldpc_decode needs for this batch / schedule. */
+int ldpc_workspace_size(const ldpc_graph_t* g, const ldpc_sched_t* s, int64_t B, size_t* bytes);
+
+/* Decode B frames.  Device outputs (row-major, per frame):
+ *   u_hat[B][N] int8 (total < 0, schedules.py:147), props[B] int64 (C2V
+ *   propagations; iterations_used = props / E), converged[B] uint8,
+ *   counters[B][8] int64 (order of _engine.py:17-25), biterr[B][i_max+1] and
+ *   biterr_info[B][i_max+1] int32 (E:191-207), kappa_hits/kappa_trials
+ *   [B][i_max] int32 (CIRBP only; may be NULL for other kinds). */
+int ldpc_decode(const ldpc_graph_t* g, const void* llr, int64_t B, const ldpc_sched_t* s,
+                int8_t* u_hat, int64_t* props, uint8_t* converged, int64_t* counters,
+                int32_t* biterr, int32_t* biterr_info, int32_t* kappa_hits, int32_t* kappa_trials,
+                void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/* Algorithm-4 VN selection (schedules.py:60-79, E:292-352) on the device:
+ * ci[N] float64, mask[N] uint8 (NULL = all), out[n_p] int32; *count_dev gets
+ * the number selected.  One warp; for API parity and tests. */
+int ldpc_select_vns(const double* ci, const uint8_t* mask, int32_t N, int32_t n_g, int32_t n_p,
+                    int64_t seed, int32_t* out, int32_t* count_dev, void* cuda_stream);
+
+/* Number of kernel launches the last ldpc_decode on this thread issued. */
+int ldpc_last_launch_count(void);
+
+const char* ldpc_strerror(int code);
+int ldpc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDPC_B200_H */

@@ -1,0 +1,557 @@
+// ldpc_capi.cu -- C ABI (include/ldpc_b200.h): graph handle, workspace sizing,
+// launch policy and kernel dispatch for the sm_100a decoder.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ldpc_b200.h"
+#include "dyn_engine.cuh"
+#include "fixed_engine.cuh"
+#include "kernel_table.h"
+
+using namespace ldpc;
+
+struct ldpc_graph {
+  DevGraph d;
+  int* dev_block;  // one allocation for every device array
+  int max_dv, max_dc, max_items;
+};
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+inline int cuda_check(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "ldpc_b200: CUDA error %s\n", cudaGetErrorString(e));
+    return LDPC_ERR_CUDA;
+  }
+  return LDPC_OK;
+}
+
+bool is_dynamic(int kind) { return kind != KIND_FLOODING && kind != KIND_LAYERED; }
+
+__host__ __device__ inline long long align16(long long x) { return (x + 15) & ~15ll; }
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int smem_optin() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (n <= 0) n = 227 * 1024;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------- dynamic engine
+
+struct DynPlan {
+  DynParams p;
+  bool smem;
+  int warps_per_block;
+  int blocks;
+  long long ws_bytes;  // including the 256-byte header (work counter)
+  int smem_bytes;
+};
+
+template <typename T>
+void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
+  using Key = typename Num<T>::Key;
+  const long long E = G->d.E, N = G->d.N;
+  const long long np = std::max(1, s->n_p);
+  long long o = 0;
+  auto take = [&](long long bytes) {
+    long long r = o;
+    o = align16(o + bytes);
+    return r;
+  };
+  p.o_c2v = take(E * sizeof(T));
+  p.o_pre = take(E * sizeof(T));
+  p.o_in = take(E * sizeof(T));
+  p.o_res = take(E * sizeof(T));
+  p.o_total = take(N * sizeof(T));
+  p.o_pretot = take(N * sizeof(T));
+  p.o_ci = take(N * sizeof(T));
+  p.rgeo = make_tree((int)E);
+  p.cgeo = make_tree((int)N);
+  const bool rt = s->kind == KIND_RBP || s->kind == KIND_CIRBP || s->kind == KIND_ME_RBP;
+  const bool ct = s->kind == KIND_CIRBP;
+  p.o_rtree = take(rt ? p.rgeo.total * (long long)sizeof(Key) : 0);
+  p.o_ctree = take(ct ? p.cgeo.total * (long long)sizeof(Key) : 0);
+  p.o_mark = 0;
+  p.o_inpp = take(N);
+  const bool me = s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP || s->kind == KIND_ME_RBP;
+  p.o_members = take(me ? std::max(N, np) * 4 : 0);
+  p.o_sel = take(me ? np * 4 : 0);
+  p.o_chosen = take(me ? np * 4 : 0);
+  p.o_tmp = take(s->kind == KIND_ME_RBP ? np * sizeof(T) : 0);
+  p.slot_bytes = align16(o);
+  // per-warp shared scratch
+  long long so = 0;
+  auto stake = [&](long long bytes) {
+    long long r = so;
+    so = align16(so + bytes);
+    return r;
+  };
+  const long long dl = std::max<long long>(G->max_items + 2, np + 1);
+  p.so_items = (int)stake((long long)G->max_items * 4);
+  p.so_itemab = (int)stake((long long)G->max_items * 8);
+  p.so_dl0 = (int)stake(dl * 4);
+  p.so_dl1 = (int)stake(dl * 4);
+  p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
+  p.scratch_bytes = (int)align16(so);
+}
+
+template <typename T>
+void* pick_dyn_kernel(int kernel, bool smem) {
+  return sizeof(T) == 8 ? ldpc_dyn_kernel_f64(kernel, smem) : ldpc_dyn_kernel_f32(kernel, smem);
+}
+
+template <typename T>
+void* pick_fixed_kernel(int kernel) {
+  return ldpc_fixed_kernel(sizeof(T) == 8, kernel);
+}
+
+template <typename T>
+int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& pl) {
+  memset(&pl, 0, sizeof(pl));
+  DynParams& p = pl.p;
+  dyn_layout<T>(G, s, p);
+  const int optin = smem_optin() - 1024;
+  const long long per_warp = p.slot_bytes + p.scratch_bytes;
+  pl.smem = !s->force_global && per_warp <= optin;
+  if (pl.smem) {
+    int w = (int)std::min<long long>(8, optin / per_warp);
+    if (per_warp > 56 * 1024) w = 1;  // let several 1-warp CTAs share an SM
+    pl.warps_per_block = std::max(1, w);
+    pl.smem_bytes = (int)(per_warp * pl.warps_per_block);
+  } else {
+    pl.warps_per_block = 8;
+    pl.smem_bytes = p.scratch_bytes * pl.warps_per_block;
+  }
+  void* fn = pick_dyn_kernel<T>(s->kernel, pl.smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.warps_per_block * 32, pl.smem_bytes) != cudaSuccess || occ < 1)
+    occ = 1;
+  long long blocks = (long long)occ * sm_count();
+  long long max_warps = B;
+  if (s->max_resident > 0) max_warps = std::min<long long>(max_warps, s->max_resident);
+  if (!pl.smem) {
+    // bound the HBM slot pool to ~24 GB
+    long long cap = std::max<long long>(1, (24ll << 30) / p.slot_bytes);
+    max_warps = std::min(max_warps, cap);
+  }
+  long long need_blocks = (max_warps + pl.warps_per_block - 1) / pl.warps_per_block;
+  blocks = std::max<long long>(1, std::min(blocks, need_blocks));
+  pl.blocks = (int)blocks;
+  pl.ws_bytes = 256 + (pl.smem ? 0 : blocks * pl.warps_per_block * p.slot_bytes);
+  return LDPC_OK;
+}
+
+// ------------------------------------------------------------ fixed engine
+
+struct FixedPlan {
+  FixedParams p;
+  int threads, blocks;
+  long long ws_bytes;
+};
+
+template <typename T>
+int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPlan& pl) {
+  memset(&pl, 0, sizeof(pl));
+  int F = 32;
+  while (F > 1 && F / 2 >= B) F /= 2;
+  pl.p.F = F;
+  pl.p.log2F = 0;
+  while ((1 << pl.p.log2F) < F) ++pl.p.log2F;
+  pl.p.slot_bytes = align16((2ll * G->d.N + G->d.E) * F * sizeof(T));
+  pl.threads = 256;
+  void* fn = pick_fixed_kernel<T>(s->kernel);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  long long groups = (B + F - 1) / F;
+  long long blocks = std::min<long long>((long long)occ * sm_count(), groups);
+  if (s->max_resident > 0) blocks = std::min<long long>(blocks, std::max(1, s->max_resident / F));
+  long long cap = std::max<long long>(1, (24ll << 30) / pl.p.slot_bytes);
+  blocks = std::max<long long>(1, std::min(blocks, cap));
+  pl.blocks = (int)blocks;
+  pl.ws_bytes = 256 + blocks * pl.p.slot_bytes;
+  return LDPC_OK;
+}
+
+int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
+  if (!G || !s || B < 0) return LDPC_ERR_INVALID;
+  if (s->kind < 0 || s->kind > KIND_ME_RBP) return LDPC_ERR_INVALID;
+  if (s->kernel != KERNEL_EXACT && s->kernel != KERNEL_MINSUM) return LDPC_ERR_INVALID;
+  if (!(s->gamma >= 0.0 && s->gamma < 1.0)) return LDPC_ERR_INVALID;  // schedules.py:37-38
+  if (s->n_p < 1 || s->n_g < 1) return LDPC_ERR_INVALID;              // schedules.py:39-40
+  if (s->i_max < 0) return LDPC_ERR_INVALID;                          // schedules.py:41-42
+  if (s->precision != LDPC_F64 && s->precision != LDPC_F32) return LDPC_ERR_INVALID;
+  if ((s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && s->n_p > G->d.N)
+    return LDPC_ERR_INVALID;  // schedules.py:136-137
+  if (is_dynamic(s->kind) && G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
+  if (!is_dynamic(s->kind) && G->max_dc > kFixedMaxDc) return LDPC_ERR_UNSUPPORTED;
+  if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
+  return LDPC_OK;
+}
+
+template <typename T>
+int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sched_t* s,
+                int8_t* u_hat, int64_t* props, uint8_t* conv, int64_t* counters, int32_t* biterr,
+                int32_t* biterr_info, int32_t* kh, int32_t* kt, void* ws, size_t ws_bytes,
+                cudaStream_t st) {
+  g_last_launches = 0;
+  if (B == 0) return LDPC_OK;
+  unsigned long long* next = (unsigned long long*)ws;
+  if (is_dynamic(s->kind)) {
+    DynPlan pl;
+    dyn_plan<T>(G, s, B, pl);
+    if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
+    if (s->kind == KIND_CIRBP && (!kh || !kt)) return LDPC_ERR_INVALID;
+    DynParams& p = pl.p;
+    p.g = G->d;
+    p.kind = s->kind;
+    p.kernel = s->kernel;
+    p.i_max = s->i_max;
+    p.n_p = s->n_p;
+    p.n_g = s->n_g;
+    p.k_info = s->k_info;
+    p.gamma = s->gamma;
+    p.seed = s->selection_seed;
+    p.llr = llr;
+    p.llr_f64 = s->llr_f64;
+    p.B = B;
+    p.u_hat = u_hat;
+    p.prop = (long long*)props;
+    p.conv = conv;
+    p.counters = (long long*)counters;
+    p.biterr = biterr;
+    p.biterr_info = biterr_info;
+    p.kh = kh;
+    p.kt = kt;
+    p.next = next;
+    p.ws = (unsigned char*)ws + 256;
+    if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
+    void* fn = pick_dyn_kernel<T>(s->kernel, pl.smem);
+    void* args[] = {&p};
+    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,
+                                             pl.smem_bytes, st)))
+      return rc;
+    g_last_launches = 1;
+  } else {
+    FixedPlan pl;
+    fixed_plan<T>(G, s, B, pl);
+    if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
+    FixedParams& p = pl.p;
+    p.g = G->d;
+    p.kind = s->kind;
+    p.kernel = s->kernel;
+    p.i_max = s->i_max;
+    p.k_info = s->k_info;
+    p.llr = llr;
+    p.llr_f64 = s->llr_f64;
+    p.B = B;
+    p.u_hat = u_hat;
+    p.prop = (long long*)props;
+    p.conv = conv;
+    p.counters = (long long*)counters;
+    p.biterr = biterr;
+    p.biterr_info = biterr_info;
+    p.next = next;
+    p.ws = (unsigned char*)ws + 256;
+    if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
+    if (int rc = cuda_check(cudaMemsetAsync(conv, 0, B, st))) return rc;
+    void* fn = pick_fixed_kernel<T>(s->kernel);
+    void* args[] = {&p};
+    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.threads), args, 0, st)))
+      return rc;
+    g_last_launches = 1;
+  }
+  return LDPC_OK;
+}
+
+// ------------------------------------------------------------ select_vns
+
+__global__ void select_vns_kernel(const double* ci, const uint8_t* mask, int N, int n_g, int n_p,
+                                  long long seed, int* out, int* count_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Ctx<double> c;
+  memset(&c, 0, sizeof(c));
+  c.lane = threadIdx.x & 31;
+  c.ci = const_cast<double*>(ci);
+  c.sizes = (int*)smem;
+  c.members = (int*)(smem + align16((long long)n_g * 4));
+  uint8_t* excl = (uint8_t*)(smem + align16((long long)n_g * 4) + align16((long long)(N > n_p ? N : n_p) * 4));
+  c.rng = seed;
+  for (int n = c.lane; n < N; n += 32) excl[n] = mask ? (mask[n] ? 0 : 1) : 0;
+  __syncwarp();
+  DynParams p;
+  memset(&p, 0, sizeof(p));
+  p.g.N = N;
+  p.n_g = n_g;
+  int cnt = select_vns<double>(p, c, excl, n_p, out);
+  if (c.lane == 0) *count_out = cnt;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+int ldpc_version(void) { return 10000; }
+
+int ldpc_last_launch_count(void) { return g_last_launches; }
+
+const char* ldpc_strerror(int code) {
+  switch (code) {
+    case LDPC_OK: return "ok";
+    case LDPC_ERR_INVALID: return "invalid argument";
+    case LDPC_ERR_UNSUPPORTED: return "graph or configuration exceeds a kernel limit";
+    case LDPC_ERR_CUDA: return "CUDA runtime error";
+    case LDPC_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int32_t* cn_ptr,
+                      const int32_t* vn_ptr, const int32_t* vn_edges, int32_t N, int32_t M,
+                      int32_t E, ldpc_graph_t** out) {
+  if (!out || N <= 0 || M <= 0 || E <= 0 || !edge_cn || !edge_vn || !cn_ptr || !vn_ptr || !vn_edges)
+    return LDPC_ERR_INVALID;
+  *out = nullptr;
+  // validate the CSR/CSC contract of build_tanner (codes.py:251-275)
+  if (cn_ptr[0] != 0 || cn_ptr[M] != E || vn_ptr[0] != 0 || vn_ptr[N] != E) return LDPC_ERR_INVALID;
+  for (int e = 0; e < E; ++e) {
+    if (edge_cn[e] < 0 || edge_cn[e] >= M || edge_vn[e] < 0 || edge_vn[e] >= N) return LDPC_ERR_INVALID;
+    if (e > 0 && (edge_cn[e] < edge_cn[e - 1] || (edge_cn[e] == edge_cn[e - 1] && edge_vn[e] <= edge_vn[e - 1])))
+      return LDPC_ERR_INVALID;  // edges must be in strictly increasing (check, vn) order
+  }
+  for (int m = 0; m < M; ++m)
+    for (int e = cn_ptr[m]; e < cn_ptr[m + 1]; ++e)
+      if (e < 0 || e >= E || edge_cn[e] != m) return LDPC_ERR_INVALID;
+  for (int n = 0; n < N; ++n)
+    for (int k = vn_ptr[n]; k < vn_ptr[n + 1]; ++k) {
+      int e = vn_edges[k];
+      if (e < 0 || e >= E || edge_vn[e] != n) return LDPC_ERR_INVALID;
+      if (k > vn_ptr[n] && vn_edges[k] <= vn_edges[k - 1]) return LDPC_ERR_INVALID;
+    }
+  ldpc_graph* G = new ldpc_graph();
+  int max_dv = 0, max_dc = 0;
+  for (int n = 0; n < N; ++n) max_dv = std::max(max_dv, vn_ptr[n + 1] - vn_ptr[n]);
+  for (int m = 0; m < M; ++m) max_dc = std::max(max_dc, cn_ptr[m + 1] - cn_ptr[m]);
+  // largest two-hop set (pre-C2V refresh size) over all edges
+  std::vector<long long> hop(N, 0);
+  for (int n = 0; n < N; ++n)
+    for (int k = vn_ptr[n]; k < vn_ptr[n + 1]; ++k) {
+      int i = edge_cn[vn_edges[k]];
+      hop[n] += cn_ptr[i + 1] - cn_ptr[i] - 1;
+    }
+  long long max_items = max_dc;
+  for (int e = 0; e < E; ++e) {
+    int i = edge_cn[e];
+    max_items = std::max(max_items, hop[edge_vn[e]] - (cn_ptr[i + 1] - cn_ptr[i] - 1));
+  }
+  // layered dependency levels: level(m) = 1 + max level of earlier checks sharing a VN
+  std::vector<int> last(N, 0), level(M, 0);
+  int n_levels = 0;
+  for (int m = 0; m < M; ++m) {
+    int lv = 0;
+    for (int e = cn_ptr[m]; e < cn_ptr[m + 1]; ++e) lv = std::max(lv, last[edge_vn[e]]);
+    level[m] = lv + 1;
+    for (int e = cn_ptr[m]; e < cn_ptr[m + 1]; ++e) last[edge_vn[e]] = lv + 1;
+    n_levels = std::max(n_levels, lv + 1);
+  }
+  std::vector<int> level_ptr(n_levels + 1, 0), level_checks(M);
+  for (int m = 0; m < M; ++m) level_ptr[level[m]]++;
+  for (int l = 0; l < n_levels; ++l) level_ptr[l + 1] += level_ptr[l];
+  {
+    std::vector<int> fillp(level_ptr.begin(), level_ptr.end() - 1);
+    for (int m = 0; m < M; ++m) level_checks[fillp[level[m] - 1]++] = m;
+  }
+  // packed records and per-edge two-hop facts for the dynamic engine
+  std::vector<int> ecv(2ull * E), vrec(2ull * N), vadj(4ull * E), hop_n(E), hop_distinct(E);
+  std::vector<uint8_t> hop_dup(E, 0);
+  for (int e = 0; e < E; ++e) {
+    ecv[2 * e] = edge_cn[e];
+    ecv[2 * e + 1] = edge_vn[e];
+  }
+  for (int n = 0; n < N; ++n) {
+    vrec[2 * n] = vn_ptr[n];
+    vrec[2 * n + 1] = vn_ptr[n + 1] - vn_ptr[n];
+    for (int k = vn_ptr[n]; k < vn_ptr[n + 1]; ++k) {
+      int f = vn_edges[k], i = edge_cn[f];
+      vadj[4 * k] = f;
+      vadj[4 * k + 1] = i;
+      vadj[4 * k + 2] = cn_ptr[i];
+      vadj[4 * k + 3] = cn_ptr[i + 1];
+    }
+  }
+  {
+    std::vector<int> stamp(N, -1);
+    for (int e = 0; e < E; ++e) {
+      int m_star = edge_cn[e], n_star = edge_vn[e], cnt = 0, distinct = 0;
+      for (int k = vn_ptr[n_star]; k < vn_ptr[n_star + 1]; ++k) {
+        int i = edge_cn[vn_edges[k]];
+        if (i == m_star) continue;
+        for (int g2 = cn_ptr[i]; g2 < cn_ptr[i + 1]; ++g2) {
+          int j = edge_vn[g2];
+          if (j == n_star) continue;
+          ++cnt;
+          if (stamp[j] != e) {
+            stamp[j] = e;
+            ++distinct;
+          }
+        }
+      }
+      hop_n[e] = cnt;
+      hop_distinct[e] = distinct;
+      hop_dup[e] = distinct < cnt ? 1 : 0;
+    }
+  }
+  // one device block (int units): edge_cn, edge_vn, vn_edges [E]; cn_ptr [M+1];
+  // vn_ptr [N+1]; level_ptr [L+1]; level_checks [M]; ecv [2E]; vrec [2N];
+  // vadj [4E] (16-byte aligned); hop_n [E]; hop_distinct [E]; hop_dup [E bytes]
+  size_t base_ints = 3ull * E + (M + 1) + (N + 1) + (n_levels + 1) + M;
+  base_ints = (base_ints + 3) & ~size_t(3);
+  size_t total = base_ints + 2ull * E + 2ull * N + 4ull * E + 2ull * E + (E + 3) / 4 + 4;
+  int* d = nullptr;
+  if (cudaMalloc(&d, total * sizeof(int)) != cudaSuccess) {
+    delete G;
+    return LDPC_ERR_CUDA;
+  }
+  std::vector<int> h(total);
+  size_t o = 0;
+  auto put = [&](const int* src, size_t n) {
+    size_t r = o;
+    memcpy(h.data() + o, src, n * sizeof(int));
+    o += n;
+    return r;
+  };
+  size_t oc = put(edge_cn, E), ov = put(edge_vn, E), oe = put(vn_edges, E);
+  size_t ocp = put(cn_ptr, M + 1), ovp = put(vn_ptr, N + 1);
+  size_t olp = put(level_ptr.data(), n_levels + 1), olc = put(level_checks.data(), M);
+  o = base_ints;
+  size_t oecv = put(ecv.data(), 2ull * E), ovrec = put(vrec.data(), 2ull * N);
+  o = (o + 3) & ~size_t(3);
+  size_t ovadj = put(vadj.data(), 4ull * E);
+  size_t ohn = put(hop_n.data(), E), ohd = put(hop_distinct.data(), E);
+  size_t ohdup = o;
+  memcpy(h.data() + o, hop_dup.data(), E);
+  if (cudaMemcpy(d, h.data(), total * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    delete G;
+    return LDPC_ERR_CUDA;
+  }
+  G->dev_block = d;
+  G->max_dv = max_dv;
+  G->max_dc = max_dc;
+  G->max_items = (int)max_items;
+  DevGraph& dg = G->d;
+  dg.N = N;
+  dg.M = M;
+  dg.E = E;
+  dg.max_dv = max_dv;
+  dg.max_dc = max_dc;
+  dg.max_items = (int)max_items;
+  dg.edge_cn = d + oc;
+  dg.edge_vn = d + ov;
+  dg.vn_edges = d + oe;
+  dg.cn_ptr = d + ocp;
+  dg.vn_ptr = d + ovp;
+  dg.n_levels = n_levels;
+  dg.level_ptr = d + olp;
+  dg.level_checks = d + olc;
+  dg.ecv = (const int2*)(d + oecv);
+  dg.vrec = (const int2*)(d + ovrec);
+  dg.vadj = (const int4*)(d + ovadj);
+  dg.hop_n = d + ohn;
+  dg.hop_distinct = d + ohd;
+  dg.hop_dup = (const uint8_t*)(d + ohdup);
+  *out = G;
+  return LDPC_OK;
+}
+
+int ldpc_graph_destroy(ldpc_graph_t* G) {
+  if (!G) return LDPC_ERR_INVALID;
+  cudaFree(G->dev_block);
+  delete G;
+  return LDPC_OK;
+}
+
+int ldpc_graph_info(const ldpc_graph_t* G, int64_t* o) {
+  if (!G || !o) return LDPC_ERR_INVALID;
+  o[0] = G->d.N;
+  o[1] = G->d.M;
+  o[2] = G->d.E;
+  o[3] = G->max_dv;
+  o[4] = G->max_dc;
+  o[5] = G->max_items;
+  o[6] = G->d.n_levels;
+  return LDPC_OK;
+}
+
+int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B, size_t* bytes) {
+  if (int rc = validate(G, s, B)) return rc;
+  if (!bytes) return LDPC_ERR_INVALID;
+  long long ws = 256;
+  if (B > 0) {
+    if (is_dynamic(s->kind)) {
+      DynPlan pl;
+      if (s->precision == LDPC_F64) dyn_plan<double>(G, s, B, pl);
+      else dyn_plan<float>(G, s, B, pl);
+      ws = pl.ws_bytes;
+    } else {
+      FixedPlan pl;
+      if (s->precision == LDPC_F64) fixed_plan<double>(G, s, B, pl);
+      else fixed_plan<float>(G, s, B, pl);
+      ws = pl.ws_bytes;
+    }
+  }
+  *bytes = (size_t)ws;
+  return LDPC_OK;
+}
+
+int ldpc_decode(const ldpc_graph_t* G, const void* llr, int64_t B, const ldpc_sched_t* s,
+                int8_t* u_hat, int64_t* props, uint8_t* converged, int64_t* counters,
+                int32_t* biterr, int32_t* biterr_info, int32_t* kappa_hits, int32_t* kappa_trials,
+                void* workspace, size_t ws_bytes, void* stream) {
+  if (int rc = validate(G, s, B)) return rc;
+  if (B > 0 && (!llr || !u_hat || !props || !converged || !counters || !biterr || !biterr_info || !workspace))
+    return LDPC_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (s->precision == LDPC_F64)
+    return decode_impl<double>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
+                               kappa_hits, kappa_trials, workspace, ws_bytes, st);
+  return decode_impl<float>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
+                            kappa_hits, kappa_trials, workspace, ws_bytes, st);
+}
+
+int ldpc_select_vns(const double* ci, const uint8_t* mask, int32_t N, int32_t n_g, int32_t n_p,
+                    int64_t seed, int32_t* out, int32_t* count_dev, void* stream) {
+  if (!ci || !out || !count_dev || N <= 0 || n_g < 1 || n_p < 1 || n_g > 4096) return LDPC_ERR_INVALID;
+  long long smem = align16((long long)n_g * 4) + align16((long long)std::max(N, n_p) * 4) + align16(N);
+  if (smem > smem_optin()) return LDPC_ERR_UNSUPPORTED;
+  cudaFuncSetAttribute((void*)select_vns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  select_vns_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(ci, mask, N, n_g, n_p, seed, out, count_dev);
+  g_last_launches = 1;
+  return cuda_check(cudaGetLastError());
+}
+
+}  // extern "C"

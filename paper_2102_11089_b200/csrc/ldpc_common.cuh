@@ -35,9 +35,17 @@ struct DevGraph {
   int n_levels;
   const int* level_ptr;     // [n_levels+1]
   const int* level_checks;  // [M]
+  // packed records for the dynamic engine (one load instead of a dependent chain)
+  const int2* ecv;          // [E]  (check, vn) of edge e
+  const int2* vrec;         // [N]  (vn_ptr[n], degree of n)
+  const int4* vadj;         // [E]  per vn_edges slot k: (f, check i of f, cn_ptr[i], cn_ptr[i+1])
+  const int* hop_n;         // [E]  two-hop set size of e (pre-C2V refreshes when e propagates)
+  const int* hop_distinct;  // [E]  distinct VNs in that set (E:536-549 candidate count)
+  const uint8_t* hop_dup;   // [E]  1 if a VN repeats in that set (4-cycle through n*)
 };
 
-// 32-ary max-tree geometry over `n` leaves (levels 1..L; level L has <= 32 nodes).
+// 32-ary max-tree geometry over `n` leaves (levels 1..L; level L has <= 64 nodes,
+// scanned two per lane).
 struct TreeGeom {
   int levels;                      // number of internal levels (>= 1)
   int size[kMaxTreeLevels + 1];    // size[0] = leaves
@@ -55,7 +63,7 @@ inline TreeGeom make_tree(int n) {
     t.size[l] = s;
     t.off[l] = tot;
     tot += s;
-  } while (t.size[l] > 32 && l < kMaxTreeLevels);
+  } while (t.size[l] > 64 && l < kMaxTreeLevels);
   t.levels = l;
   t.total = tot;
   return t;
@@ -164,12 +172,17 @@ __device__ __forceinline__ unsigned warp_max_key(unsigned k, int* lane_out) {
 }
 
 // Max key with the smallest companion index among ties (index < 2^31).
-template <typename K>
-__device__ __forceinline__ K warp_max_key_minidx(K k, int idx, int* idx_out) {
-  int ln;
-  K m = warp_max_key(k, &ln);
-  unsigned cand = (k == m) ? (unsigned)idx : 0xffffffffu;
-  *idx_out = (int)__reduce_min_sync(kFull, cand);
+__device__ __forceinline__ unsigned long long warp_max_key_minidx(unsigned long long k, int idx,
+                                                                  int* idx_out) {
+  unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  unsigned mh = __reduce_max_sync(kFull, hi);
+  unsigned ml = __reduce_max_sync(kFull, (hi == mh) ? lo : 0u);
+  *idx_out = (int)__reduce_min_sync(kFull, (hi == mh && lo == ml) ? (unsigned)idx : 0xffffffffu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned warp_max_key_minidx(unsigned k, int idx, int* idx_out) {
+  unsigned m = __reduce_max_sync(kFull, k);
+  *idx_out = (int)__reduce_min_sync(kFull, (k == m) ? (unsigned)idx : 0xffffffffu);
   return m;
 }
 

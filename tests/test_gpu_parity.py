@@ -1,0 +1,131 @@
+"""GPU parity: the sm_100a decoder (through the C ABI) against the reference.
+
+* golden vectors (produced by the reference itself) -- every schedule, kernel
+  and config in tests/golden/*.npz;
+* seeded batches against the CPU oracle (pinned to the reference) -- the
+  north-star bar: >= 99.9% of frames identical (hard decisions and update
+  counts), float64;
+* the two schedules the reference lacks (layered, ME-RBP) against the oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pyoracle
+from paper_2102_11089_b200.channel import llr_batch
+from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch, results_to_numpy
+from tests.util import golden_cases, golden_digest_ok, load_code
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("u_hat", "prop", "converged", "counters", "bit_errors_at", "info_bit_errors_at")
+
+
+def _cfg(sched, **kw):
+    d = dict(kind="flooding", gamma=0.1, n_p=1, n_g=16, i_max=3, kernel="exact", selection_seed=0)
+    d.update(sched)
+    d.update(kw)
+    return ScheduleConfig(**d)
+
+
+def _gpu(spec, llrs, cfg, **kw):
+    t = torch.from_numpy(np.ascontiguousarray(llrs)).cuda()
+    out = decode_batch(spec, t, cfg, **kw)
+    torch.cuda.synchronize()
+    return results_to_numpy(out, cfg.kind, cfg.i_max)
+
+
+@pytest.mark.parametrize("fname,code_key,si,sched", golden_cases())
+def test_gpu_matches_reference_golden(fname, code_key, si, sched):
+    z = np.load(f"tests/golden/{fname}.npz")
+    spec, g = load_code(code_key)
+    assert golden_digest_ok(fname, g)
+    cfg = _cfg(sched)
+    got = _gpu(spec, z["llrs"], cfg)
+    t = f"s{si}"
+    ok = ((np.packbits(got["u_hat"].astype(np.uint8), axis=1) == z[f"{t}_u_hat"]).all(1)
+          & (got["prop"] == z[f"{t}_prop"])
+          & (got["converged"] == z[f"{t}_converged"])
+          & (got["counters"] == z[f"{t}_counters"]).all(1)
+          & (got["bit_errors_at"] == z[f"{t}_biterr"]).all(1)
+          & (got["info_bit_errors_at"] == z[f"{t}_biterr_info"]).all(1))
+    if cfg.kind == "cirbp":
+        ok &= (got["kappa_hits_iter"] == z[f"{t}_kh"]).all(1)
+        ok &= (got["kappa_trials_iter"] == z[f"{t}_kt"]).all(1)
+    bad = np.flatnonzero(~ok)
+    assert len(bad) == 0, f"{sched}: frames {bad.tolist()} differ from the reference"
+
+
+def _compare_oracle(spec, g, llrs, cfg, min_frac=0.999):
+    got = _gpu(spec, llrs, cfg)
+    ref = pyoracle.decode_batch(g, llrs.astype(np.float64), cfg.kind, cfg.kernel, cfg.i_max,
+                                spec.k_info, cfg.gamma, cfg.n_p, cfg.n_g, cfg.selection_seed)
+    same = (got["u_hat"] == ref["u_hat"]).all(1) & (got["prop"] == ref["prop"])
+    full = same & (got["counters"] == ref["counters"]).all(1) & \
+        (got["bit_errors_at"] == ref["bit_errors_at"]).all(1) & (got["converged"] == ref["converged"])
+    assert same.mean() >= min_frac, f"{cfg}: {same.mean():.4f} identical"
+    return same, full
+
+
+@pytest.mark.parametrize("kind", ["flooding", "layered", "rbp", "cirbp", "lmdrbp", "slmdrbp",
+                                  "lmd_cirbp", "me_cirbp", "me_lmd_cirbp", "me_rbp"])
+def test_c0_batch_vs_oracle(kind):
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=0, start=1000, count=2000)
+    _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 5, "n_p": 4}))
+
+
+@pytest.mark.parametrize("kind", ["layered", "rbp", "cirbp", "lmd_cirbp", "me_cirbp", "me_rbp"])
+def test_c1_batch_vs_oracle(kind):
+    spec, g = load_code("C1")
+    llrs = llr_batch(spec, 2.0, seed=0, start=0, count=1000)
+    _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 3, "n_p": 4}))
+
+
+@pytest.mark.parametrize("kind,n_p", [("layered", 1), ("rbp", 1), ("cirbp", 1), ("me_cirbp", 16)])
+def test_c2_batch_vs_oracle(kind, n_p):
+    spec, g = load_code("C2")
+    llrs = llr_batch(spec, 1.0, seed=0, start=0, count=64)
+    _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 3, "n_p": n_p}), min_frac=0.98)
+
+
+@pytest.mark.parametrize("kind", ["flooding", "layered", "rbp", "me_rbp"])
+def test_minsum_and_new_schedules(kind):
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.5, seed=3, start=0, count=500)
+    _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 5, "kernel": "minsum", "n_p": 4}))
+
+
+@pytest.mark.parametrize("kind", ["rbp", "cirbp", "lmd_cirbp", "flooding"])
+def test_global_state_mode_matches(kind):
+    """HBM-resident frame state (the big-code path) gives the same answers."""
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=0, start=5000, count=300)
+    cfg = _cfg({"kind": kind, "i_max": 5})
+    a = _gpu(spec, llrs, cfg)
+    b = _gpu(spec, llrs, cfg, force_global=True)
+    for k in FIELDS:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_small_batches_and_imax0():
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=0, start=0, count=3)
+    for kind in ("rbp", "flooding", "me_cirbp", "lmdrbp"):
+        for i_max in (0, 1):
+            _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": i_max, "n_p": 4}), min_frac=1.0)
+    empty = _gpu(spec, llrs[:0], _cfg({"kind": "rbp"}))
+    assert empty["prop"].shape == (0,)
+
+
+def test_fp32_mode_statistics():
+    """fp32 fast mode: same decoder, FER within noise of the float64 path."""
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=0, start=0, count=4000)
+    a = _gpu(spec, llrs, _cfg({"kind": "cirbp", "i_max": 5}))
+    b = _gpu(spec, llrs, _cfg({"kind": "cirbp", "i_max": 5, "precision": "f32"}))
+    fa = (a["bit_errors_at"][:, -1] > 0).mean()
+    fb = (b["bit_errors_at"][:, -1] > 0).mean()
+    assert abs(fa - fb) < 4 * np.sqrt(fa * (1 - fa) / len(llrs)) + 1e-3
+    assert ((a["u_hat"] == b["u_hat"]).all(1)).mean() > 0.95
