@@ -72,7 +72,8 @@ typedef struct {
   int32_t precision;      /* LDPC_F64 / LDPC_F32 */
   int32_t llr_f64;        /* 0: llr is float32[B][N], 1: float64[B][N] */
   int32_t max_resident;   /* 0 = auto; else cap on concurrently decoded frames */
-  int32_t force_global;   /* 1 = keep frame state in HBM even if it fits in smem */
+  int32_t placement;      /* dynamic schedules: 0 auto, 1 all state in HBM, 2 per-edge state in HBM,
+                             3 all in shared memory, 4 per-edge + per-VN state in HBM (trees in smem) */
 } ldpc_sched_t;
 
 /* Build the device-resident Tanner graph (edge ids in (check, vn) order,
@@ -105,6 +106,20 @@ int ldpc_decode(const ldpc_graph_t* g, const void* llr, int64_t B, const ldpc_sc
  * the number selected.  One warp; for API parity and tests. */
 int ldpc_select_vns(const double* ci, const uint8_t* mask, int32_t N, int32_t n_g, int32_t n_p,
                     int64_t seed, int32_t* out, int32_t* count_dev, void* cuda_stream);
+
+/* Debug / near-tie tracing: subsequent ldpc_decode calls on this thread write,
+ * for each of the first `cap` updates k of frame f, the propagated edge to
+ * dev_log[2 * (f * cap + k)] and the committed C2V value (float64 bits) to
+ * dev_log[2 * (f * cap + k) + 1] (dynamic schedules only; the caller fills
+ * the buffer with -1).  cap = 0 disables. */
+int ldpc_set_step_log(int64_t* dev_log, int32_t cap);
+
+/* Debug: subsequent dynamic-schedule decodes on this thread copy frame 0's
+ * state right before update `step` into dev_buf (float64): ci[N] and
+ * pre_total[N] at [0, 2N) (CI schedules), the RNG state after each Alg.-4
+ * selection at [2N, 2N+8192), pre[E] and c2v[E] at [2N+8192, 2N+8192+2E).
+ * step < 0 disables. */
+int ldpc_set_state_dump(int64_t step, double* dev_buf);
 
 /* Number of kernel launches the last ldpc_decode on this thread issued. */
 int ldpc_last_launch_count(void);

@@ -229,9 +229,15 @@ static int64_t argmax_vn_edges(const real* res, const graph_t* g, int64_t n) {
 
 /* ------------------------------------------------------ near-tie logging */
 
+/* relative top-2 gap; values under GAP_FLOOR sit at the float64 noise floor of
+ * the messages (1 ulp of a +-30 LLR is 3.6e-15), so the gap is taken relative
+ * to max(best, GAP_FLOOR) */
+#define GAP_FLOOR 1e-8
 static inline void gap_note(state_t* s, double best, double second) {
   if (!s->log) return;
-  double gap = best > 0 ? (best - second) / best : (best == second ? 0.0 : 1.0);
+  if (second < 0) second = 0;
+  double den = best > GAP_FLOOR ? best : GAP_FLOOR;
+  double gap = (best - second) / den;
   if (gap < s->cur_gap) s->cur_gap = gap;
 }
 
@@ -258,6 +264,22 @@ static void gap_vn_edges(state_t* s, const real* res, const graph_t* g, int64_t 
   gap_note(s, b, c);
 }
 
+/* test-only state dump: ci[] and pre_total[] before update `g_dump_step` */
+static int64_t g_dump_step = -1;
+static double *g_dump_ci = NULL, *g_dump_pt = NULL;
+static int64_t g_dump_n = 0;
+static double *g_dump_pre = NULL, *g_dump_c2v = NULL;
+static int64_t g_dump_e = 0;
+void or_set_dump_edges(double* pre, double* c2v, int64_t e) { g_dump_pre = pre; g_dump_c2v = c2v; g_dump_e = e; }
+void or_set_dump(int64_t step, double* ci, double* pt, int64_t n) {
+  g_dump_step = step; g_dump_ci = ci; g_dump_pt = pt; g_dump_n = n;
+}
+/* test-only: RNG state after each Alg.-4 selection */
+static int64_t* g_rng_log = NULL;
+static int64_t g_rng_cap = 0, g_rng_len = 0;
+void or_set_rng_log(int64_t* buf, int64_t cap) { g_rng_log = buf; g_rng_cap = cap; g_rng_len = 0; }
+int64_t or_rng_log_len(void) { return g_rng_len; }
+
 static inline void log_step(state_t* s, int64_t e, real c2v) {
   steplog_t* L = s->log;
   if (!L) return;
@@ -274,6 +296,10 @@ static inline void log_step(state_t* s, int64_t e, real c2v) {
 
 static void propagate(int64_t e_star, const graph_t* g, int kernel, state_t* s, int maintain_ci,
                       tree_t* res_tree, tree_t* ci_tree) {
+  if (s->log && s->log->len == g_dump_step && g_dump_ci)
+    for (int64_t n = 0; n < g_dump_n; ++n) { g_dump_ci[n] = (double)s->ci[n]; g_dump_pt[n] = (double)s->pre_total[n]; }
+  if (s->log && s->log->len == g_dump_step && g_dump_pre)
+    for (int64_t e = 0; e < g_dump_e; ++e) { g_dump_pre[e] = (double)s->pre[e]; g_dump_c2v[e] = (double)s->c2v[e]; }
   int64_t m_star = g->edge_cn[e_star];
   int64_t n_star = g->edge_vn[e_star];
   real old = s->c2v[e_star];
@@ -371,8 +397,22 @@ static inline int64_t ci_group(real c, int n_g) {
   return gi;
 }
 
+/* near-tie note for Alg. 4: relative distance of ci*n_g to the nearest group
+ * boundary, minimised over the candidate VNs (logging only) */
+static void gap_groups(state_t* s, const real* ci, const int8_t* mask, int64_t n_vars, int n_g) {
+  if (!s || !s->log) return;
+  for (int64_t n = 0; n < n_vars; ++n) {
+    if (!mask[n]) continue;
+    double x = (double)ci[n] * n_g, r = floor(x + 0.5);
+    if (r < 1.0 || r > n_g - 1) continue;
+    double g = fabs(x - r) / r;
+    if (g < s->cur_gap) s->cur_gap = g;
+  }
+}
+
 static int64_t select_vns(const real* ci, const int8_t* mask, int64_t n_vars, int n_g, int n_p,
-                          int64_t* rng, int64_t* out) {
+                          int64_t* rng, int64_t* out, state_t* st) {
+  gap_groups(st, ci, mask, n_vars, n_g);
   int64_t* sizes = (int64_t*)calloc((size_t)n_g, sizeof(int64_t));
   for (int64_t n = 0; n < n_vars; ++n)
     if (mask[n]) sizes[ci_group(ci[n], n_g)]++;
@@ -402,6 +442,7 @@ static int64_t select_vns(const real* ci, const int8_t* mask, int64_t n_vars, in
     }
     free(mem);
   }
+  if (g_rng_log && st && g_rng_len < g_rng_cap) g_rng_log[g_rng_len++] = *rng;
   /* sort ascending (insertion sort: count <= n_p) */
   for (int64_t a = 1; a < count; ++a) {
     int64_t v = out[a], b = a - 1;
@@ -638,7 +679,7 @@ static int64_t decode_me_cirbp(const graph_t* g, const sched_t* c, state_t* s, i
   int64_t* sel = (int64_t*)malloc(sizeof(int64_t) * (size_t)c->n_p);
   *conv = 0;
   while (boundary <= c->i_max && !*conv) {
-    int64_t count = select_vns(s->ci, mask, N, c->n_g, c->n_p, &rng, sel);
+    int64_t count = select_vns(s->ci, mask, N, c->n_g, c->n_p, &rng, sel, s);
     s->counters[C_MSEL] += c->n_g;
     for (int64_t idx = 0; idx < count; ++idx) {
       int64_t p = sel[idx];
@@ -666,7 +707,7 @@ static int64_t decode_me_lmd_cirbp(const graph_t* g, const sched_t* c, state_t* 
   int8_t* in_pp = (int8_t*)calloc((size_t)N, 1);
   uint8_t* seen = (uint8_t*)calloc((size_t)N, 1);
   *conv = 0;
-  int64_t count = select_vns(s->ci, mask, N, c->n_g, c->n_p, &rng, sel);
+  int64_t count = select_vns(s->ci, mask, N, c->n_g, c->n_p, &rng, sel, s);
   s->counters[C_MSEL] += c->n_g;
   while (boundary <= c->i_max && !*conv) {
     for (int64_t idx = 0; idx < count; ++idx) {
@@ -691,7 +732,7 @@ static int64_t decode_me_lmd_cirbp(const graph_t* g, const sched_t* c, state_t* 
     }
     if (npc < c->n_p) {
       for (int64_t n = 0; n < N; ++n) mask[n] = (int8_t)(1 - in_pp[n]);
-      int64_t extra = select_vns(s->ci, mask, N, c->n_g, (int)(c->n_p - npc), &rng, sel + npc);
+      int64_t extra = select_vns(s->ci, mask, N, c->n_g, (int)(c->n_p - npc), &rng, sel + npc, s);
       s->counters[C_MSEL] += c->n_g;
       count = npc + extra;
     } else {
@@ -725,7 +766,15 @@ static int64_t decode_me_rbp(const graph_t* g, const sched_t* c, state_t* s, int
       sel[b] = e;
       if (cnt < np_) cnt++;
     }
-    if (s->log && np_ == 1) gap_all(s, s->res, E);
+    if (s->log && cnt < E) {  /* near-tie at the selection boundary: n_p-th vs (n_p+1)-th */
+      double lo = s->res[sel[cnt - 1]], hi = -1;
+      for (int64_t e = 0; e < E; ++e) {
+        int in = 0;
+        for (int64_t q = 0; q < cnt; ++q) in |= sel[q] == e;
+        if (!in && s->res[e] > hi) hi = s->res[e];
+      }
+      gap_note(s, lo, hi);
+    }
     s->counters[C_CMP] += E - 1;
     for (int64_t a = 1; a < cnt; ++a) {
       int64_t v = sel[a], b = a - 1;
@@ -944,7 +993,7 @@ int64_t or_select_vns(const double* ci_in, const int8_t* mask, int64_t n_vars, i
   real* ci = (real*)malloc(sizeof(real) * (size_t)n_vars);
   for (int64_t n = 0; n < n_vars; ++n) ci[n] = (real)ci_in[n];
   int64_t rng = seed;
-  int64_t r = select_vns(ci, mask, n_vars, n_g, n_p, &rng, out);
+  int64_t r = select_vns(ci, mask, n_vars, n_g, n_p, &rng, out, NULL);
   free(ci);
   return r;
 }

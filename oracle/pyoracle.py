@@ -47,6 +47,13 @@ def lib(single=False):
                                        C.c_int, _I64] + [_P] * 8)
         L.or_select_vns.restype = _I64
         L.or_select_vns.argtypes = [_P, _P, _I64, C.c_int, C.c_int, _I64, _P]
+        L.or_set_dump_edges.restype = None
+        L.or_set_dump_edges.argtypes = [_P, _P, _I64]
+        L.or_set_rng_log.restype = None
+        L.or_set_rng_log.argtypes = [_P, _I64]
+        L.or_rng_log_len.restype = _I64
+        L.or_set_dump.restype = None
+        L.or_set_dump.argtypes = [_I64, _P, _P, _I64]
         L.or_rand_next.restype = _I64
         L.or_rand_next.argtypes = [_P]
         _LIBS[key] = L
@@ -151,3 +158,27 @@ def rand_next(state):
     st = np.array([_seed64(state)], np.int64)
     z = lib().or_rand_next(_p(st))
     return int(z), int(st[0])
+
+
+def decode_dump(g, chl, step, **kw):
+    """decode() with the oracle's ci / pre_total captured before update `step`."""
+    L = lib(kw.get("single", False))
+    ci = np.zeros(g.n_vars)
+    pt = np.zeros(g.n_vars)
+    rng = np.zeros(8192, np.int64)
+    pre = np.zeros(g.n_edges)
+    c2v = np.zeros(g.n_edges)
+    L.or_set_dump_edges(_p(pre), _p(c2v), g.n_edges)
+    L.or_set_dump(step, _p(ci), _p(pt), g.n_vars)
+    L.or_set_rng_log(_p(rng), len(rng))
+    try:
+        kw.setdefault("log_cap", step + 2)
+        r = decode(g, chl, **kw)
+        nr = L.or_rng_log_len()
+    finally:
+        L.or_set_dump(-1, None, None, 0)
+        L.or_set_dump_edges(None, None, 0)
+        L.or_set_rng_log(None, 0)
+    r["dump_ci"], r["dump_pretot"], r["rng_log"] = ci, pt, rng[:nr]
+    r["dump_pre"], r["dump_c2v"] = pre, c2v
+    return r

@@ -7,28 +7,36 @@
 //   plus ME-RBP (new; defined in oracle/ldpc_oracle.c).
 //
 // Design (B200):
-//  * a persistent grid; each warp pulls frame ids from an atomic work queue,
-//    so a frame that converges early frees its warp for the next frame;
-//  * a frame's whole message state lives in one "slot": in shared memory when
-//    it fits (small codes), else in a per-warp HBM slot that stays hot in L2;
-//  * the update (_propagate, E:130-176) is latency-bound and serial per
-//    frame, so the kernel minimises its dependent-load chain: packed graph
-//    records (edge -> (check, vn); VN slot -> (f, check, check range)) and
-//    per-edge precomputed two-hop facts (size, distinct VNs, duplicates);
-//  * lanes compute the V2C messages of M(n*)\m*, then the two-hop pre-C2V
-//    refresh packs all (d_v-1)(d_c-1) edges across the 32 lanes; pre_total
-//    accumulations that hit the same VN (4-cycles through n*) are applied in
-//    the reference's order (match_any ranks), so float64 results are
-//    bit-identical;
-//  * global argmax uses 32-ary max trees of order-preserving integer keys; the
-//    argmax descends with one coalesced load + REDUX.MAX per level (lowest
-//    index wins ties, like the reference's left-preferring segment tree,
-//    E:220-257); after an update only the touched 32-leaf groups and their
-//    ancestors are recomputed, one node per lane, level-synchronously.
+//  * persistent grid; each warp pulls frame ids from an atomic work queue, so a
+//    frame that converges early frees its warp for the next frame;
+//  * a frame's state is split in two parts placed by the host (MODE):
+//      per-edge part  c2v, pre, in (= tanh(v2c/2) or v2c) [, res]   E x 3-4 words
+//      per-VN part    total [, pre_total, ci], trees, ME scratch    N x 1-3 words
+//    MODE 0: both in shared memory; MODE 1: per-edge part in an L2-resident
+//    HBM slot, per-VN part in shared memory; MODE 2: both in HBM (huge codes);
+//  * the residual is never stored: it is |pre - c2v| exactly (E:144,167), so
+//    tree leaves are recomputed from pre and c2v; for RBP-family schedules
+//    pre_total / CI are not maintained (the reference keeps them only for its
+//    trace output, E:171-176);
+//  * the update (_propagate, E:130-176) is a latency-bound serial chain, so it
+//    is built to minimise dependent memory round trips: packed graph records,
+//    per-edge precomputed two-hop facts, each touched check's inputs staged
+//    once into shared memory, then all (d_v-1)(d_c-1) pre-C2V refreshes run
+//    lane-parallel with the reference's exact product order;
+//  * pre_total accumulations that hit the same VN (4-cycle through n*) are
+//    applied in the reference's order (match_any ranks), so float64 results
+//    are bit-identical;
+//  * global argmax: 32-ary max trees of order-preserving integer keys, one
+//    coalesced load + REDUX.MAX per level, lowest index wins ties like the
+//    reference's left-preferring segment tree (E:220-257); only the touched
+//    32-leaf groups and their ancestors are recomputed.  Small CI vectors are
+//    scanned flat instead.
 #pragma once
 #include "ldpc_common.cuh"
 
 namespace ldpc {
+
+constexpr int kFlatCiMax = 1024;  // CIRBP: flat CI argmax when N <= this
 
 struct DynParams {
   DevGraph g;
@@ -48,96 +56,119 @@ struct DynParams {
   int* kh;                // [B][i_max] (CIRBP)
   int* kt;
   unsigned long long* next;
-  // per-frame state slots
-  unsigned char* ws;
-  long long slot_bytes;
-  long long o_c2v, o_pre, o_in, o_res, o_total, o_pretot, o_ci, o_rtree, o_ctree, o_mark,
-      o_inpp, o_members, o_sel, o_chosen, o_tmp;
+  long long* step_log;    // debug: propagated edge of the first log_cap updates per frame
+  int log_cap;
+  int dbg_full_tree;      // debug: recompute every touched tree group from its leaves
+  long long dump_step;    // debug: copy ci / pre_total of frame 0 before this update
+  double* dump_buf;       // [2N]
+  // state placement: per-edge (E), per-VN (N) and tree (T) parts
+  unsigned char* ws;      // HBM slots
+  long long slotE_bytes, slotN_bytes, slotT_bytes;
+  long long o_c2v, o_pre, o_in, o_res;                           // E part
+  long long o_total, o_pretot, o_ci, o_p0t, o_inpp, o_members, o_sel, o_chosen, o_tmp;  // N part
+  long long o_rtree, o_ridx, o_ctree, o_cidx;                    // T part
   TreeGeom rgeo, cgeo;
-  int scratch_bytes;  // per-warp shared scratch
-  int so_items, so_itemab, so_dl0, so_dl1, so_sizes;
+  int flat_ci;            // CIRBP: flat CI argmax instead of a tree
+  int scratch_bytes;      // per-warp shared scratch
+  int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes;
 };
 
 template <typename T>
 struct Ctx {
   using Key = typename Num<T>::Key;
-  T *c2v, *pre, *in, *res, *total, *pretot, *ci, *tmp;
-  Key *rtree, *ctree;
+  T *c2v, *pre, *in, *res, *total, *pretot, *ci, *p0t, *tmp;  // p0t = p0(total), CI kinds
+  Key *rtree, *ctree;  // tree node keys, all levels
+  int *ridx, *cidx;    // level-1 argmax leaf of each 32-leaf group
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
   int *members, *sel, *chosen;
-  int* items;     // two-hop edge ids of the last update, ascending
-  int2* itemab;   // check range [a, b) of each item
+  int4* items;    // two-hop edges of the last update (g, a, d, stage base), ascending g
+  T* stage;       // staged check inputs of the last update
+  Key* nk;        // new residual key of each item
   int *dl0, *dl1; // dirty-node lists for tree maintenance
   int* sizes;     // Alg.4 group histogram
   long long cnt[kCounters];
   long long prop;
+  long long cur_f;   // frame being decoded
+  int nsel;          // Alg.-4 selections made (debug log index)
   long long next_b;  // next single-edge iteration boundary (k * E)
-  int it;            // completed iterations (= prop / E, maintained incrementally)
+  int it;            // completed iterations
   int lane;
   long long rng;
 };
 
-// ------------------------------------------------------------- max trees
+// residual leaf key: |pre - c2v| (or the stored residual for ME-RBP's exclusion)
+template <typename T, bool STORED>
+__device__ __forceinline__ typename Num<T>::Key res_key(const Ctx<T>& c, int e) {
+  if (STORED) return Num<T>::key(c.res[e]);
+  return Num<T>::key(Num<T>::abs_(c.pre[e] - c.c2v[e]));
+}
 
-template <typename T>
-__device__ __forceinline__ typename Num<T>::Key child_key(const typename Num<T>::Key* tree,
-                                                          const T* leaves, const TreeGeom& geo,
-                                                          int level, int child) {
-  if (child >= geo.size[level]) return 0;
-  if (level == 0) return Num<T>::key(leaves[child]);
+// ------------------------------------------------------------- max trees
+// Node keys for levels 1..L (tree + off[l]); level 1 also stores the index of
+// its maximal leaf (lowest index among equal keys), so an argmax descent ends
+// in shared memory without touching the leaves.  LeafFn: int -> Key.
+
+template <typename Key, typename LeafFn>
+__device__ __forceinline__ Key child_key(const Key* tree, const TreeGeom& geo, int level, int child,
+                                         LeafFn leaf) {
+  if (child >= geo.size[level]) return Key(0);
+  if (level == 0) return leaf(child);
   return tree[geo.off[level] + child];
 }
 
-// max over the 32 children of node q at level l (children at l-1), staggered by lane
-template <typename T>
-__device__ __forceinline__ typename Num<T>::Key node_max(const typename Num<T>::Key* tree,
-                                                         const T* leaves, const TreeGeom& geo,
-                                                         int l, int q, int lane) {
-  using Key = typename Num<T>::Key;
-  Key m = 0;
-  const int base = q * 32, lim = geo.size[l - 1] - base;
-  if (l == 1) {
-#pragma unroll 8
-    for (int c = 0; c < 32; ++c) {
-      int ch = (c + lane) & 31;
-      Key k = ch < lim ? Num<T>::key(leaves[base + ch]) : Key(0);
-      m = k > m ? k : m;
-    }
-  } else {
-    const Key* row = tree + geo.off[l - 1] + base;
-#pragma unroll 8
-    for (int c = 0; c < 32; ++c) {
-      int ch = (c + lane) & 31;
-      Key k = ch < lim ? row[ch] : Key(0);
-      m = k > m ? k : m;
-    }
-  }
-  return m;
+__device__ __forceinline__ unsigned long long warp_max_only(unsigned long long k) {
+  unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  unsigned mh = __reduce_max_sync(kFull, hi);
+  unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+  return ((unsigned long long)mh << 32) | ml;
 }
+__device__ __forceinline__ unsigned warp_max_only(unsigned k) { return __reduce_max_sync(kFull, k); }
 
-template <typename T>
-__device__ void tree_build(typename Num<T>::Key* tree, const T* leaves, const TreeGeom& geo, int lane) {
-  for (int l = 1; l <= geo.levels; ++l) {
-    for (int q = lane; q < geo.size[l]; q += 32) tree[geo.off[l] + q] = node_max<T>(tree, leaves, geo, l, q, lane);
-    __syncwarp();
+template <typename Key, typename LeafFn>
+__device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, int lane, LeafFn leaf) {
+  for (int q = lane; q < geo.size[1]; q += 32) {
+    Key m = 0;
+    int bi = q * 32;
+    for (int c = 0; c < 32; ++c) {
+      Key k = child_key(tree, geo, 0, q * 32 + c, leaf);
+      if (k > m) { m = k; bi = q * 32 + c; }
+    }
+    tree[geo.off[1] + q] = m;
+    idx1[q] = bi;
   }
-}
-
-// Recompute the level-1 nodes in dl[0..n) and all their ancestors.
-// Duplicates in dl are harmless (same value written twice).
-template <typename T>
-__device__ void tree_update_list(typename Num<T>::Key* tree, const T* leaves, const TreeGeom& geo,
-                                 int* dl, int* dl2, int n, int lane) {
-  for (int l = 1; l <= geo.levels; ++l) {
-    for (int base = 0; base < n; base += 32) {
-      int idx = base + lane;
-      if (idx < n) {
-        int q = dl[idx];
-        tree[geo.off[l] + q] = node_max<T>(tree, leaves, geo, l, q, lane);
+  __syncwarp();
+  for (int l = 2; l <= geo.levels; ++l) {
+    for (int q = lane; q < geo.size[l]; q += 32) {
+      Key m = 0;
+      for (int c = 0; c < 32; ++c) {
+        Key k = child_key(tree, geo, l - 1, q * 32 + c, leaf);
+        m = k > m ? k : m;
       }
+      tree[geo.off[l] + q] = m;
     }
     __syncwarp();
-    if (l == geo.levels) break;
+  }
+}
+
+// Full recompute of level-1 group q from its leaves (warp-cooperative).
+template <typename Key, typename LeafFn>
+__device__ __forceinline__ void group_recompute(Key* tree, int* idx1, const TreeGeom& geo, int q, int lane,
+                                                LeafFn leaf) {
+  int e = q * 32 + lane;
+  Key k = child_key(tree, geo, 0, e, leaf);
+  int best;
+  Key m = warp_max_key_minidx(k, e, &best);
+  if (lane == 0) {
+    tree[geo.off[1] + q] = m;
+    idx1[q] = best;
+  }
+}
+
+// Recompute the ancestors (levels >= 2) of the level-1 groups dl[0..n).
+template <typename Key, typename LeafFn>
+__device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int* dl2, int n, int lane,
+                                   LeafFn leaf) {
+  for (int l = 2; l <= geo.levels; ++l) {
     int cnt = 0;
     for (int base = 0; base < n; base += 32) {
       int idx = base + lane;
@@ -153,38 +184,104 @@ __device__ void tree_update_list(typename Num<T>::Key* tree, const T* leaves, co
     dl = dl2;
     dl2 = t;
     n = cnt;
+    for (int i = 0; i < n; ++i) {
+      int q = dl[i];
+      Key m = warp_max_only(child_key(tree, geo, l - 1, q * 32 + lane, leaf));
+      if (lane == 0) tree[geo.off[l] + q] = m;
+    }
+    __syncwarp();
   }
 }
 
-template <typename T>
-__device__ int tree_argmax(const typename Num<T>::Key* tree, const T* leaves, const TreeGeom& geo,
-                           int lane) {
-  using Key = typename Num<T>::Key;
+// Full recompute of the level-1 groups dl[0..n) and their ancestors.
+template <typename Key, typename LeafFn>
+__device__ void tree_update_list(Key* tree, int* idx1, const TreeGeom& geo, int* dl, int* dl2, int n,
+                                 int lane, LeafFn leaf) {
+  for (int i = 0; i < n; ++i) group_recompute(tree, idx1, geo, dl[i], lane, leaf);
+  __syncwarp();
+  tree_fix_ancestors(tree, geo, dl, dl2, n, lane, leaf);
+}
+
+// Incremental rule for one leaf e of group q getting key kk, applied to the
+// group's (max key Q, argmax I): returns true if the group must be recomputed
+// (its argmax leaf decreased).
+template <typename Key>
+__device__ __forceinline__ bool leaf_rule(Key& Q, int& I, int e, Key kk) {
+  if (kk > Q) {
+    Q = kk;
+    I = e;
+  } else if (kk == Q) {
+    if (e < I) I = e;
+  } else if (e == I) {
+    return true;
+  }
+  return false;
+}
+
+// Incremental update of level-1 groups for per-lane leaf changes (leaf e or
+// -1, new key kk), lanes of the same group serialised by a match_any leader.
+// Appends groups to recompute to rec[] and changed groups to dirty[].
+template <typename Key>
+__device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Key kk, int lane, int* se,
+                                                   Key* sk, int* rec, int& nrec, int* dirty, int& ndirty) {
+  const int q = e >= 0 ? (e >> 5) : -1;
+  se[lane] = e;
+  sk[lane] = kk;
+  __syncwarp();
+  const unsigned peers = __match_any_sync(kFull, q);
+  const bool leader = e >= 0 && (__ffs(peers) - 1) == lane;
+  bool r = false, changed = false;
+  if (leader) {
+    Key Q = L1[q];
+    int I = idx1[q];
+    const Key Q0 = Q;
+    const int I0 = I;
+    unsigned m = peers;
+    while (m && !r) {
+      const int s2 = __ffs(m) - 1;
+      m &= m - 1;
+      r = leaf_rule(Q, I, se[s2], sk[s2]);
+    }
+    if (!r && (Q != Q0 || I != I0)) {
+      L1[q] = Q;
+      idx1[q] = I;
+    }
+    changed = r || Q != Q0;
+  }
+  const unsigned rb = __ballot_sync(kFull, r), cb = __ballot_sync(kFull, changed);
+  if (r) rec[nrec + __popc(rb & lanemask_lt())] = q;
+  if (changed) dirty[ndirty + __popc(cb & lanemask_lt())] = q;
+  nrec += __popc(rb);
+  ndirty += __popc(cb);
+  __syncwarp();
+}
+
+template <typename Key, typename LeafFn>
+__device__ int tree_argmax(const Key* tree, const int* idx1, const TreeGeom& geo, int lane, LeafFn leaf) {
   const int L = geo.levels, s = geo.size[L];
   const Key* top = tree + geo.off[L];
   Key k0 = lane < s ? top[lane] : Key(0);
   Key k1 = lane + 32 < s ? top[lane + 32] : Key(0);
   int q;
   warp_max_key_minidx(k1 > k0 ? k1 : k0, k1 > k0 ? lane + 32 : lane, &q);
-  for (int l = L - 1; l >= 0; --l) {
-    Key k = child_key<T>(tree, leaves, geo, l, q * 32 + lane);
+  for (int l = L - 1; l >= 1; --l) {
+    Key k = child_key(tree, geo, l, q * 32 + lane, leaf);
     int ln;
     warp_max_key(k, &ln);
     q = q * 32 + ln;
   }
-  return q;
+  return idx1[q];
 }
 
 // ------------------------------------------------------------ argmax scans
 
-// E:260-266 -- first maximum over values[0..n)
-template <typename T>
-__device__ int argmax_all(const T* v, int n, int lane) {
-  using Key = typename Num<T>::Key;
+// E:260-266 -- first maximum of key(i) over i in [0, n)
+template <typename Key, typename KeyFn>
+__device__ int argmax_scan(int n, int lane, KeyFn keyf) {
   Key best = 0;
   int bi = 0x7fffffff;
   for (int i = lane; i < n; i += 32) {
-    Key k = Num<T>::key(v[i]);
+    Key k = keyf(i);
     if (k > best) { best = k; bi = i; }
   }
   int idx;
@@ -194,11 +291,11 @@ __device__ int argmax_all(const T* v, int n, int lane) {
 
 // E:269-276 -- first maximum residual over M(n) in vn_edges order (= edge order)
 template <typename T>
-__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const T* res, int n, int lane) {
+__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T>& c, int n, int lane) {
   using Key = typename Num<T>::Key;
   int2 vr = g.vrec[n];
   int e = lane < vr.y ? g.vn_edges[vr.x + lane] : 0x7fffffff;
-  Key k = lane < vr.y ? Num<T>::key(res[e]) : Key(0);
+  Key k = lane < vr.y ? res_key<T, false>(c, e) : Key(0);
   int idx;
   warp_max_key_minidx(k, e, &idx);
   return idx;
@@ -206,25 +303,24 @@ __device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const T* res, 
 
 // ------------------------------------------------------- two-hop item table
 
-// Items = {g in N(i)\{f} : f in M(n*), i = cn(f) != m*}, in ascending edge id
-// (= the reference's scan order, E:153-166 / E:450-460).  `adj` is this lane's
-// vadj record (lane < d_v) and `act` says whether its check is != m*.
+// Items = {g in N(i)\{f} : f in M(n*), i = cn(f) != m*}, ascending edge id (the
+// reference's scan order, E:153-166 / E:450-460).  `adj` is this lane's vadj
+// record (lane < d_v), `act` = its check is not m*.  Also lays out the stage
+// area: check k's inputs at stage[sbase_k + (e - a_k)].  Returns the count;
+// the caller must __syncwarp() before reading the table.
 template <typename T>
-__device__ __forceinline__ int build_items_from(Ctx<T>& c, int4 adj, bool act) {
-  int cnt = act ? adj.w - adj.z - 1 : 0;
-  int incl = warp_incl_scan(cnt);
-  int total = __shfl_sync(kFull, incl, 31);
+__device__ __forceinline__ int build_items_from(Ctx<T>& c, int4 adj, bool act, int* sbase_out) {
+  const int d = act ? adj.w - adj.z : 0;
+  const int packed = act ? ((d - 1) | (d << 16)) : 0;
+  const int incl = warp_incl_scan(packed);
+  const int total = __shfl_sync(kFull, incl, 31) & 0xffff;
+  const int t0 = (incl - packed) & 0xffff, sbase = (incl - packed) >> 16;
   if (act) {
-    int t = incl - cnt;
-    const int2 ab = make_int2(adj.z, adj.w);
+    int t = t0;
     for (int e = adj.z; e < adj.w; ++e)
-      if (e != adj.x) {
-        c.items[t] = e;
-        c.itemab[t] = ab;
-        ++t;
-      }
+      if (e != adj.x) c.items[t++] = make_int4(e, adj.z, d, sbase);
   }
-  __syncwarp();
+  *sbase_out = sbase;
   return total;
 }
 
@@ -234,98 +330,225 @@ __device__ int build_items(const DevGraph& g, Ctx<T>& c, int e_star) {
   int2 vr = g.vrec[mn.y];
   int4 adj = make_int4(-1, -1, 0, 0);
   if (c.lane < vr.y) adj = g.vadj[vr.x + c.lane];
-  return build_items_from<T>(c, adj, c.lane < vr.y && adj.y != mn.x);
+  int sb;
+  int n = build_items_from<T>(c, adj, c.lane < vr.y && adj.y != mn.x, &sb);
+  __syncwarp();
+  return n;
 }
 
 // ------------------------------------------------------------- propagate
 
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
-// pre-C2V / residual / pre_total (/ CI) state.  Leaves the item table of e*.
-template <typename T, int KERNEL, bool CI, bool RT, bool CT>
+// pre-C2V (and, for CI schedules, pre_total / CI) state.  Leaves the item
+// table of e* for the LMD searches.
+template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED>
 __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
+  using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
   const int lane = c.lane;
-  const int2 mn = g.ecv[e_star];
-  const int m_star = mn.x, n_star = mn.y;
-  const int2 vr = g.vrec[n_star];
+  const int4 er = g.erec[e_star];  // (m*, n*, vn_ptr[n*], d_v(n*))
+  const int m_star = er.x, n_star = er.y;
+  const int2 vr = make_int2(er.z, er.w);
   int4 adj = make_int4(-1, -1, 0, 0);
   if (lane < vr.y) adj = g.vadj[vr.x + lane];
   const bool act = lane < vr.y && adj.y != m_star;
   const T old = c.c2v[e_star];
   const T nv = c.pre[e_star];
   const T tot = c.total[n_star] + (nv - old);  // E:147
-  T cf = act ? c.c2v[adj.x] : T(0);
-  const bool dup = g.hop_dup[e_star] != 0;
+  const T cf = act ? c.c2v[adj.x] : T(0);
+  if (p.dump_buf && c.cur_f == 0 && c.prop == p.dump_step) {
+    if (CI)
+      for (int n = lane; n < g.N; n += 32) {
+        p.dump_buf[n] = (double)c.ci[n];
+        p.dump_buf[g.N + n] = (double)c.pretot[n];
+      }
+    for (int e = lane; e < g.E; e += 32) {
+      p.dump_buf[2 * g.N + 8192 + e] = (double)c.pre[e];
+      p.dump_buf[2 * g.N + 8192 + g.E + e] = (double)c.c2v[e];
+    }
+  }
   __syncwarp();
   if (lane == 0) {
+    if (p.step_log && c.prop < p.log_cap) {  // (edge, committed value bits) pairs
+      p.step_log[2 * (c.cur_f * p.log_cap + c.prop)] = e_star;
+      p.step_log[2 * (c.cur_f * p.log_cap + c.prop) + 1] = __double_as_longlong((double)nv);
+    }
     c.c2v[e_star] = nv;
-    c.res[e_star] = T(0);
+    if (STORED) c.res[e_star] = T(0);
     c.total[n_star] = tot;
-    if (CI) c.ci[n_star] = ci_of(tot, c.pretot[n_star]);  // E:148-149
+    if (CI) {
+      const T pt = p0(tot);  // cached p0(total) of n*, the only total that changes
+      c.p0t[n_star] = pt;
+      c.ci[n_star] = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
+    }
   }
-  if (act) {  // V2C to the other checks of n* (E:153-160)
+  int sbase;
+  const int n_items = build_items_from<T>(c, adj, act, &sbase);
+  if (act) {  // V2C to the other checks of n* (E:153-160), also staged
     T v = clampv(tot - cf);
-    c.in[adj.x] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+    T th = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+    c.in[adj.x] = th;
+    c.stage[sbase + (adj.x - adj.z)] = th;
   }
-  const int n_items = build_items_from<T>(c, adj, act);  // ends with __syncwarp
+  __syncwarp();
+  for (int t = lane; t < n_items; t += 32) {  // stage the rest of each check
+    int4 r = c.items[t];
+    c.stage[r.w + (r.x - r.y)] = c.in[r.x];
+  }
+  __syncwarp();
+  const bool dup = CI && g.hop_dup[e_star] != 0;
   // two-hop refresh (E:161-176), 32 edges per pass in reference order
   for (int base = 0; base < n_items; base += 32) {
     const int t = base + lane;
     const bool valid = t < n_items;
-    int ge = -1, j = -1;
+    int j = -1;
     T delta = T(0);
     if (valid) {
-      ge = c.items[t];
-      const int2 ab = c.itemab[t];
-      j = g.edge_vn[ge];
-      T np_ = cn_msg_cached<T, KERNEL>(c.in, ab.x, ab.y, ge);
-      T op = c.pre[ge];
+      const int4 r = c.items[t];
+      const int ge = r.x, skip = r.x - r.y;
+      // independent loads first (the pre[] store below would otherwise pin them)
+      const T cg = c.c2v[ge];
+      T opre = T(0);
+      if (CI) {
+        j = g.edge_vn[ge];
+        opre = c.pre[ge];
+      }
+      const T* s = c.stage + r.w;
+      T np_;
+      if (KERNEL == KERNEL_EXACT) {
+        T prod = T(1);
+        for (int q = 0; q < r.z; ++q)
+          if (q != skip) prod *= s[q];
+        np_ = atanh_msg(prod, r.z - 1);
+      } else {
+        T sign = T(1), mag = Num<T>::kBig;
+        for (int q = 0; q < r.z; ++q) {
+          if (q == skip) continue;
+          T v = clampv(s[q]);
+          if (v < T(0)) { sign = -sign; v = -v; }
+          if (v < mag) mag = v;
+        }
+        np_ = r.z > 1 ? clampv(sign * mag) : T(0);
+      }
+      if (CI) delta = np_ - opre;
       c.pre[ge] = np_;
-      c.res[ge] = Num<T>::abs_(np_ - c.c2v[ge]);
-      delta = np_ - op;
+      T rv = Num<T>::abs_(np_ - cg);
+      if (STORED) c.res[ge] = rv;
+      if (RT) c.nk[t] = Num<T>::key(rv);
     }
-    if (!dup) {
-      if (valid) {
-        T pt = c.pretot[j] + delta;  // E:171
-        c.pretot[j] = pt;
-        if (CI) c.ci[j] = ci_of(c.total[j], pt);  // E:173
+    if (CI) {
+      if (!dup) {
+        if (valid) {
+          T pt = c.pretot[j] + delta;  // E:171
+          c.pretot[j] = pt;
+          c.ci[j] = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
+        }
+      } else {
+        // the same VN reached through two checks (4-cycle): keep the reference's order
+        unsigned peers = __match_any_sync(kFull, j);
+        int rank = __popc(peers & lanemask_lt());
+        int maxrank = __reduce_max_sync(kFull, valid ? (unsigned)rank : 0u);
+        for (int r = 0; r <= maxrank; ++r) {
+          if (valid && rank == r) c.pretot[j] += delta;
+          __syncwarp();
+        }
+        bool last = valid && ((peers >> lane) >> 1) == 0;
+        if (last) c.ci[j] = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
       }
-    } else {
-      // same VN reached through two checks (4-cycle): keep the reference's order
-      unsigned peers = __match_any_sync(kFull, j);
-      int rank = __popc(peers & lanemask_lt());
-      int maxrank = __reduce_max_sync(kFull, valid ? (unsigned)rank : 0u);
-      for (int r = 0; r <= maxrank; ++r) {
-        if (valid && rank == r) c.pretot[j] += delta;
-        __syncwarp();
-      }
-      bool last = valid && ((peers >> lane) >> 1) == 0;
-      if (CI && last) c.ci[j] = ci_of(c.total[j], c.pretot[j]);
     }
-    __syncwarp();
   }
-  if (RT) {  // dirty res-tree groups: items (ascending) + e*
-    int cnt = 0, prev = -1;
+  __syncwarp();
+  if (RT) {
+    // incremental residual-tree update: e* first (residual -> 0), then one
+    // leader lane per 32-leaf group of the (ascending) items applies the leaf
+    // rule; groups whose argmax leaf decreased are recomputed from leaves.
+    const TreeGeom& geo = p.rgeo;
+    Key* L1 = c.rtree + geo.off[1];
+    int nrec = 0, ndirty = 0;
+    {
+      const int q = e_star >> 5;
+      Key Q = L1[q];
+      int I = c.ridx[q];
+      const Key Q0 = Q;
+      bool rec = leaf_rule(Q, I, e_star, Num<T>::key(T(0)));
+      __syncwarp();
+      if (lane == 0) {
+        if (rec) c.dl1[nrec] = q;
+        else {
+          L1[q] = Q;
+          c.ridx[q] = I;
+        }
+        if (rec || Q != Q0) c.dl0[ndirty] = q;
+      }
+      nrec += rec ? 1 : 0;
+      ndirty += (rec || Q != Q0) ? 1 : 0;
+      __syncwarp();
+    }
     for (int base = 0; base < n_items; base += 32) {
-      int t = base + lane;
-      int gq = t < n_items ? (c.items[t] >> 5) : 0x7fffffff;
-      int up = __shfl_up_sync(kFull, gq, 1);
-      if (lane == 0) up = prev;
-      bool keep = t < n_items && gq != up;
-      unsigned bal = __ballot_sync(kFull, keep);
-      if (keep) c.dl0[cnt + __popc(bal & lanemask_lt())] = gq;
-      cnt += __popc(bal);
-      prev = __shfl_sync(kFull, gq, 31);
+      const int t = base + lane;
+      const bool valid = t < n_items;
+      const int e = valid ? c.items[t].x : -1;
+      const int q = valid ? (e >> 5) : -1;
+      const Key kk = valid ? c.nk[t] : Key(0);
+      // lanes of one group form a contiguous segment (items ascend); reduce it
+      const unsigned peers = __match_any_sync(kFull, q);
+      const bool leader = valid && (__ffs(peers) - 1) == lane;
+      Key Q = 0;
+      int I = 0;
+      if (valid) {
+        Q = L1[q];
+        I = c.ridx[q];
+      }
+      // the group's argmax leaf decreased -> recompute from leaves
+      const bool dec = valid && ((e == I && kk < Q) || p.dbg_full_tree);
+      const bool rec = __ballot_sync(kFull, dec) & peers;
+      // segment max of the new keys, lowest edge among ties
+      int bi;
+      const Key km = warp_max_key_minidx_masked(kk, e, peers, &bi);
+      bool changed = false;
+      if (leader) {
+        if (rec) changed = true;
+        else if (km > Q || (km == Q && bi < I)) {
+          changed = km > Q;
+          L1[q] = km;
+          c.ridx[q] = bi;
+        }
+      }
+      const bool lrec = leader && rec;
+      const unsigned rb = __ballot_sync(kFull, lrec), cb = __ballot_sync(kFull, changed);
+      if (lrec) c.dl1[nrec + __popc(rb & lanemask_lt())] = q;
+      if (changed) c.dl0[ndirty + __popc(cb & lanemask_lt())] = q;
+      nrec += __popc(rb);
+      ndirty += __popc(cb);
+      __syncwarp();
     }
-    if (lane == 0) c.dl0[cnt] = e_star >> 5;
+    auto rleaf = [&](int e) -> Key { return res_key<T, STORED>(c, e); };
+    for (int i = 0; i < nrec; ++i) group_recompute(c.rtree, c.ridx, geo, c.dl1[i], lane, rleaf);
     __syncwarp();
-    tree_update_list<T>(c.rtree, c.res, p.rgeo, c.dl0, c.dl1, cnt + 1, lane);
+    if (geo.levels > 1) tree_fix_ancestors(c.rtree, geo, c.dl0, c.dl1, ndirty, lane, rleaf);
   }
-  if (CT) {  // dirty ci-tree groups: two-hop VNs + n*
-    for (int t = lane; t < n_items; t += 32) c.dl0[t] = g.edge_vn[c.items[t]] >> 5;
-    if (lane == 0) c.dl0[n_items] = n_star >> 5;
+  if (CT) {  // incremental CI-tree update: n* first, then the two-hop VNs
+    const TreeGeom& geo = p.cgeo;
+    Key* L1 = c.ctree + geo.off[1];
+    int* se = (int*)c.stage;  // stage is free again: 32 (index, key) pairs
+    Key* sk = (Key*)(se + 32);
+    int nrec = 0, ndirty = 0;
+    apply_leaf_updates(L1, c.cidx, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), lane, se, sk,
+                       c.dl1, nrec, c.dl0, ndirty);
+    for (int base = 0; base < n_items; base += 32) {
+      const int t = base + lane;
+      int j = -1;
+      Key kk = 0;
+      if (t < n_items) {
+        j = g.edge_vn[c.items[t].x];
+        kk = Num<T>::key(c.ci[j]);
+      }
+      apply_leaf_updates(L1, c.cidx, j, kk, lane, se, sk, c.dl1, nrec, c.dl0, ndirty);
+    }
+    auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
+    for (int i = 0; i < nrec; ++i) group_recompute(c.ctree, c.cidx, geo, c.dl1[i], lane, cleaf);
     __syncwarp();
-    tree_update_list<T>(c.ctree, c.ci, p.cgeo, c.dl0, c.dl1, n_items + 1, lane);
+    if (geo.levels > 1) tree_fix_ancestors(c.ctree, geo, c.dl0, c.dl1, ndirty, lane, cleaf);
   }
   c.cnt[C_PROP] += 1;
   c.cnt[C_V2C] += vr.y - 1;
@@ -480,6 +703,9 @@ __device__ int select_vns(const DynParams& p, Ctx<T>& c, const uint8_t* excl, in
     count += need;
   }
   __syncwarp();
+  if (p.dump_buf && c.cur_f == 0 && lane == 0 && c.nsel < 8192)
+    p.dump_buf[2 * N + c.nsel] = __longlong_as_double(c.rng);
+  ++c.nsel;
   // ascending sort of out[0..count) (distinct VN ids): rank sort through members[]
   for (int i = lane; i < count; i += 32) {
     int v = out[i], r = 0;
@@ -522,14 +748,14 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T>& c, int e_prev, int n_it
     ncand = b - a - 1;
     for (int e = a + lane; e < b; e += 32)
       if (e != e_prev) {
-        Key k = Num<T>::key(c.res[e]);
+        Key k = res_key<T, false>(c, e);
         if (k > bk) { bk = k; bi = e; }
       }
   } else {
     ncand = n_items;
     for (int t = lane; t < n_items; t += 32) {
-      int e = c.items[t];
-      Key k = Num<T>::key(c.res[e]);
+      int e = c.items[t].x;
+      Key k = res_key<T, false>(c, e);
       if (k > bk) { bk = k; bi = e; }
     }
   }
@@ -539,7 +765,7 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T>& c, int e_prev, int n_it
   warp_max_key_minidx(bk, bi, &best);
   if (!simplified) {
     int np_ = g.edge_vn[best];
-    best = argmax_vn_edges<T>(g, c.res, np_, lane);
+    best = argmax_vn_edges<T>(g, c, np_, lane);
     c.cnt[C_CMP] += g.vrec[np_].y - 1;
   }
   return best;
@@ -569,7 +795,7 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T>& c, int e_prev, int n
     if (!have_items) n_items = build_items<T>(g, c, e_prev);
     ncand = g.hop_distinct[e_prev];
     for (int t = lane; t < n_items; t += 32) {
-      int j = g.edge_vn[c.items[t]];
+      int j = g.edge_vn[c.items[t].x];
       Key k = Num<T>::key(c.ci[j]);
       if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
     }
@@ -583,7 +809,7 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T>& c, int e_prev, int n
 
 // --------------------------------------------------------------- decoders
 
-template <typename T, int KERNEL>
+template <typename T, int KERNEL, bool CI>
 __device__ void init_state(const DynParams& p, Ctx<T>& c, long long f) {  // E:106-127
   const DevGraph& g = p.g;
   const int lane = c.lane;
@@ -599,61 +825,71 @@ __device__ void init_state(const DynParams& p, Ctx<T>& c, long long f) {  // E:1
   __syncwarp();
   for (int m = lane; m < g.M; m += 32) {
     int a = g.cn_ptr[m], b = g.cn_ptr[m + 1];
-    for (int e = a; e < b; ++e) {
-      T v = cn_msg_cached<T, KERNEL>(c.in, a, b, e);
-      c.pre[e] = v;
-      c.res[e] = Num<T>::abs_(v - T(0));
-    }
+    for (int e = a; e < b; ++e) c.pre[e] = cn_msg_cached<T, KERNEL>(c.in, a, b, e);
   }
   __syncwarp();
-  for (int n = lane; n < g.N; n += 32) {
-    T acc = chl(n);
-    for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
-    c.pretot[n] = acc;
-    c.ci[n] = ci_of(c.total[n], acc);
-    c.inpp[n] = 0;
-  }
+  if (CI)
+    for (int n = lane; n < g.N; n += 32) {
+      T acc = chl(n);
+      for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
+      c.pretot[n] = acc;
+      const T pt = p0(c.total[n]);
+      c.p0t[n] = pt;
+      c.ci[n] = Num<T>::abs_(pt - p0(acc));
+    }
+  if (p.kind == KIND_ME_LMD_CIRBP)
+    for (int n = lane; n < g.N; n += 32) c.inpp[n] = 0;
   __syncwarp();
 }
 
-template <typename T, int KERNEL>
+template <typename T, int KERNEL, int KF>
 __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
+  const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
+  using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
   const long long E = g.E, budget = (long long)p.i_max * E;
   const int lane = c.lane, I = p.i_max;
   for (int k = 0; k < kCounters; ++k) c.cnt[k] = 0;
   c.prop = 0;
+  c.cur_f = f;
+  c.nsel = 0;
   c.next_b = E;
   c.it = 0;
   c.rng = p.seed;
   bool conv = false;
   if (lane == 0) {
     for (int k = 0; k <= I; ++k) p.biterr[f * (I + 1) + k] = p.biterr_info[f * (I + 1) + k] = 0;
-    if (p.kind == KIND_CIRBP)
+    if (kind == KIND_CIRBP)
       for (int k = 0; k < I; ++k) p.kh[f * I + k] = p.kt[f * I + k] = 0;
   }
-  init_state<T, KERNEL>(p, c, f);
+  const bool ci_kind = kind == KIND_CIRBP || kind == KIND_LMD_CIRBP || kind == KIND_ME_CIRBP ||
+                       kind == KIND_ME_LMD_CIRBP;
+  if (ci_kind) init_state<T, KERNEL, true>(p, c, f);
+  else init_state<T, KERNEL, false>(p, c, f);
   record_boundary<T>(p, c.total, f, 0, lane);
+  auto rleaf = [&](int e) -> Key { return res_key<T, false>(c, e); };
+  auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
 
-  switch (p.kind) {
+  switch (kind) {
     case KIND_RBP: {  // E:355-385
-      tree_build<T>(c.rtree, c.res, p.rgeo, lane);
+      tree_build(c.rtree, c.ridx, p.rgeo, lane, rleaf);
       while (c.prop < budget) {
-        int e = tree_argmax<T>(c.rtree, c.res, p.rgeo, lane);
+        int e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, rleaf);
         c.cnt[C_CMP] += E - 1;
-        propagate<T, KERNEL, false, true, false>(p, c, e);
+        propagate<T, KERNEL, false, true, false, false>(p, c, e);
         ++c.prop;
         if (single_boundary<T>(p, c, f, &conv)) break;
       }
     } break;
     case KIND_CIRBP: {  // E:388-433
-      tree_build<T>(c.rtree, c.res, p.rgeo, lane);
-      tree_build<T>(c.ctree, c.ci, p.cgeo, lane);
+      tree_build(c.rtree, c.ridx, p.rgeo, lane, rleaf);
+      const bool flat = p.flat_ci != 0;
+      if (!flat) tree_build(c.ctree, c.cidx, p.cgeo, lane, cleaf);
       const T gamma = (T)p.gamma;
-      int kh = 0, kt = 0;  // per-iteration kappa tallies (lane-uniform)
+      int kh = 0, kt = 0;  // per-iteration kappa tallies (warp-uniform)
       while (c.prop < budget) {
         const int it = c.it;
-        int n_star = tree_argmax<T>(c.ctree, c.ci, p.cgeo, lane);
+        int n_star = flat ? argmax_scan<Key>(g.N, lane, cleaf) : tree_argmax(c.ctree, c.cidx, p.cgeo, lane, cleaf);
         c.cnt[C_CMP] += g.N - 1 + 1;
         c.cnt[C_KTRIALS] += 1;
         ++kt;
@@ -662,16 +898,16 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
         if (hit) {
           c.cnt[C_KHITS] += 1;
           ++kh;
-          e = tree_argmax<T>(c.rtree, c.res, p.rgeo, lane);
+          e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, rleaf);
           c.cnt[C_CMP] += E - 1;
         } else {
-          e = argmax_vn_edges<T>(g, c.res, n_star, lane);
+          e = argmax_vn_edges<T>(g, c, n_star, lane);
           c.cnt[C_CMP] += g.vrec[n_star].y - 1;
         }
-        propagate<T, KERNEL, true, true, true>(p, c, e);
+        if (flat) propagate<T, KERNEL, true, true, false, false>(p, c, e);
+        else propagate<T, KERNEL, true, true, true, false>(p, c, e);
         ++c.prop;
-        const bool at_b = c.prop == c.next_b;
-        if (at_b || c.prop >= budget) {
+        if (c.prop == c.next_b || c.prop >= budget) {
           if (lane == 0) {
             p.kh[f * I + it] = kh;
             p.kt[f * I + it] = kt;
@@ -683,38 +919,38 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
     } break;
     case KIND_LMDRBP:
     case KIND_SLMDRBP: {  // E:472-510
-      const bool simplified = p.kind == KIND_SLMDRBP;
-      int e = argmax_all<T>(c.res, g.E, lane);
+      const bool simplified = p.kind == KIND_SLMDRBP;  // sLMDRBP runs the LMDRBP kernel
+      int e = argmax_scan<Key>(g.E, lane, rleaf);
       c.cnt[C_CMP] += E - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, false, false, false>(p, c, e);
+        int n_items = propagate<T, KERNEL, false, false, false, false>(p, c, e);
         ++c.prop;
         if (single_boundary<T>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
         int en = lmd_next_edge<T>(p, c, e, n_items, simplified);
         if (en < 0) {
-          en = argmax_all<T>(c.res, g.E, lane);
+          en = argmax_scan<Key>(g.E, lane, rleaf);
           c.cnt[C_CMP] += E - 1;
         }
         e = en;
       }
     } break;
     case KIND_LMD_CIRBP: {  // E:555-598
-      int n_star = argmax_all<T>(c.ci, g.N, lane);
+      int n_star = argmax_scan<Key>(g.N, lane, cleaf);
       c.cnt[C_CMP] += g.N - 1;
-      int e = argmax_vn_edges<T>(g, c.res, n_star, lane);
+      int e = argmax_vn_edges<T>(g, c, n_star, lane);
       c.cnt[C_CMP] += g.vrec[n_star].y - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, true, false, false>(p, c, e);
+        int n_items = propagate<T, KERNEL, true, false, false, false>(p, c, e);
         ++c.prop;
         if (single_boundary<T>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
         int nn = ci_argmax_twohop<T>(p, c, e, n_items, true);
         if (nn < 0) {
-          nn = argmax_all<T>(c.ci, g.N, lane);
+          nn = argmax_scan<Key>(g.N, lane, cleaf);
           c.cnt[C_CMP] += g.N - 1;
         }
-        e = argmax_vn_edges<T>(g, c.res, nn, lane);
+        e = argmax_vn_edges<T>(g, c, nn, lane);
         c.cnt[C_CMP] += g.vrec[nn].y - 1;
       }
     } break;
@@ -725,9 +961,9 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
         c.cnt[C_MSEL] += p.n_g;
         for (int idx = 0; idx < count; ++idx) {
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T>(g, c.res, pv, lane);
+          int e = argmax_vn_edges<T>(g, c, pv, lane);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
-          propagate<T, KERNEL, true, false, false>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T>(p, c, f, &boundary, &conv);
@@ -740,10 +976,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
       while (boundary <= I && !conv) {
         for (int idx = 0; idx < count; ++idx) {
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T>(g, c.res, pv, lane);
+          int e = argmax_vn_edges<T>(g, c, pv, lane);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
           if (lane == 0) c.chosen[idx] = e;
-          propagate<T, KERNEL, true, false, false>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T>(p, c, f, &boundary, &conv);
@@ -775,13 +1011,16 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
         sort_small<T>(c, c.sel, count);
       }
     } break;
-    case KIND_ME_RBP: {  // new (oracle/ldpc_oracle.c decode_me_rbp)
-      tree_build<T>(c.rtree, c.res, p.rgeo, lane);
+    case KIND_ME_RBP: {  // new (oracle/ldpc_oracle.c decode_me_rbp): stored residuals
+      for (int e = lane; e < g.E; e += 32) c.res[e] = Num<T>::abs_(c.pre[e] - c.c2v[e]);
+      __syncwarp();
+      auto sleaf = [&](int e) -> Key { return res_key<T, true>(c, e); };
+      tree_build(c.rtree, c.ridx, p.rgeo, lane, sleaf);
       int boundary = 1;
       const int np_ = p.n_p < g.E ? p.n_p : g.E;
       while (boundary <= I && !conv) {
         for (int t = 0; t < np_; ++t) {
-          int e = tree_argmax<T>(c.rtree, c.res, p.rgeo, lane);
+          int e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, sleaf);
           if (lane == 0) {
             c.sel[t] = e;
             c.tmp[t] = c.res[e];
@@ -789,18 +1028,18 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
             c.dl0[0] = e >> 5;
           }
           __syncwarp();
-          tree_update_list<T>(c.rtree, c.res, p.rgeo, c.dl0, c.dl1, 1, lane);
+          tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, 1, lane, sleaf);
         }
         for (int t = lane; t < np_; t += 32) {
           c.res[c.sel[t]] = c.tmp[t];
           c.dl0[t] = c.sel[t] >> 5;
         }
         __syncwarp();
-        tree_update_list<T>(c.rtree, c.res, p.rgeo, c.dl0, c.dl1, np_, lane);
+        tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, np_, lane, sleaf);
         c.cnt[C_CMP] += E - 1;
         sort_small<T>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
-          propagate<T, KERNEL, false, true, false>(p, c, c.sel[idx]);
+          propagate<T, KERNEL, false, true, false, true>(p, c, c.sel[idx]);
           ++c.prop;
         }
         me_boundaries<T>(p, c, f, &boundary, &conv);
@@ -825,32 +1064,46 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
   __syncwarp();
 }
 
-template <typename T, int KERNEL, bool SMEM>
+// MODE 0: E, N and T parts in shared memory; 1: E in HBM, N and T in shared;
+// 2: E and N in HBM, T in shared; 3: everything in HBM.
+template <typename T, int KERNEL, int MODE, int KF>
 __global__ void __launch_bounds__(256) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  unsigned char* slot = SMEM ? smem + (long long)warp * p.slot_bytes
-                             : p.ws + ((long long)blockIdx.x * wpb + warp) * p.slot_bytes;
-  unsigned char* scr = smem + (SMEM ? (long long)wpb * p.slot_bytes : 0) + (long long)warp * p.scratch_bytes;
+  const long long gw = (long long)blockIdx.x * wpb + warp;
+  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes;
+  // shared bytes per warp and HBM bytes per warp for this mode
+  const long long sh = (MODE == 0 ? sE + sN + sT : MODE == 1 ? sN + sT : MODE == 2 ? sT : 0);
+  const long long hb = (MODE == 0 ? 0 : MODE == 1 ? sE : MODE == 2 ? sE + sN : sE + sN + sT);
+  unsigned char* shw = smem + warp * sh;
+  unsigned char* hbw = p.ws + gw * hb;
+  unsigned char* bE = MODE == 0 ? shw : hbw;
+  unsigned char* bN = MODE == 0 ? shw + sE : MODE == 1 ? shw : hbw + sE;
+  unsigned char* bT = MODE == 0 ? shw + sE + sN : MODE == 1 ? shw + sN : MODE == 2 ? shw : hbw + sE + sN;
+  unsigned char* scr = smem + (long long)wpb * sh + (long long)warp * p.scratch_bytes;
   using Key = typename Num<T>::Key;
   Ctx<T> c;
   c.lane = threadIdx.x & 31;
-  c.c2v = (T*)(slot + p.o_c2v);
-  c.pre = (T*)(slot + p.o_pre);
-  c.in = (T*)(slot + p.o_in);
-  c.res = (T*)(slot + p.o_res);
-  c.total = (T*)(slot + p.o_total);
-  c.pretot = (T*)(slot + p.o_pretot);
-  c.ci = (T*)(slot + p.o_ci);
-  c.tmp = (T*)(slot + p.o_tmp);
-  c.rtree = (Key*)(slot + p.o_rtree);
-  c.ctree = (Key*)(slot + p.o_ctree);
-  c.inpp = (uint8_t*)(slot + p.o_inpp);
-  c.members = (int*)(slot + p.o_members);
-  c.sel = (int*)(slot + p.o_sel);
-  c.chosen = (int*)(slot + p.o_chosen);
-  c.items = (int*)(scr + p.so_items);
-  c.itemab = (int2*)(scr + p.so_itemab);
+  c.c2v = (T*)(bE + p.o_c2v);
+  c.pre = (T*)(bE + p.o_pre);
+  c.in = (T*)(bE + p.o_in);
+  c.res = (T*)(bE + p.o_res);
+  c.total = (T*)(bN + p.o_total);
+  c.pretot = (T*)(bN + p.o_pretot);
+  c.ci = (T*)(bN + p.o_ci);
+  c.p0t = (T*)(bN + p.o_p0t);
+  c.tmp = (T*)(bN + p.o_tmp);
+  c.inpp = (uint8_t*)(bN + p.o_inpp);
+  c.members = (int*)(bN + p.o_members);
+  c.sel = (int*)(bN + p.o_sel);
+  c.chosen = (int*)(bN + p.o_chosen);
+  c.rtree = (Key*)(bT + p.o_rtree);
+  c.ridx = (int*)(bT + p.o_ridx);
+  c.ctree = (Key*)(bT + p.o_ctree);
+  c.cidx = (int*)(bT + p.o_cidx);
+  c.items = (int4*)(scr + p.so_items);
+  c.stage = (T*)(scr + p.so_stage);
+  c.nk = (Key*)(scr + p.so_nk);
   c.dl0 = (int*)(scr + p.so_dl0);
   c.dl1 = (int*)(scr + p.so_dl1);
   c.sizes = (int*)(scr + p.so_sizes);
@@ -859,7 +1112,7 @@ __global__ void __launch_bounds__(256) dyn_decode_kernel(const __grid_constant__
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);
     f = __shfl_sync(kFull, f, 0);
     if ((long long)f >= p.B) break;
-    decode_frame<T, KERNEL>(p, c, (long long)f);
+    decode_frame<T, KERNEL, KF>(p, c, (long long)f);
   }
 }
 

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -23,6 +24,10 @@ struct ldpc_graph {
 namespace {
 
 thread_local int g_last_launches = 0;
+thread_local long long* g_step_log = nullptr;
+thread_local int g_log_cap = 0;
+thread_local long long g_dump_step = -1;
+thread_local double* g_dump_buf = nullptr;
 
 inline int cuda_check(cudaError_t e) {
   if (e != cudaSuccess) {
@@ -62,45 +67,60 @@ int smem_optin() {
 
 struct DynPlan {
   DynParams p;
-  bool smem;
+  int mode;  // 0: all smem, 1: per-edge part in HBM, 2: all HBM
   int warps_per_block;
   int blocks;
   long long ws_bytes;  // including the 256-byte header (work counter)
   int smem_bytes;
 };
 
+bool ci_kind(int k) {
+  return k == KIND_CIRBP || k == KIND_LMD_CIRBP || k == KIND_ME_CIRBP || k == KIND_ME_LMD_CIRBP;
+}
+bool me_kind(int k) { return k == KIND_ME_CIRBP || k == KIND_ME_LMD_CIRBP || k == KIND_ME_RBP; }
+
 template <typename T>
 void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   using Key = typename Num<T>::Key;
   const long long E = G->d.E, N = G->d.N;
   const long long np = std::max(1, s->n_p);
+  const bool ci = ci_kind(s->kind), me = me_kind(s->kind);
   long long o = 0;
   auto take = [&](long long bytes) {
     long long r = o;
     o = align16(o + bytes);
     return r;
   };
+  // E part
   p.o_c2v = take(E * sizeof(T));
   p.o_pre = take(E * sizeof(T));
   p.o_in = take(E * sizeof(T));
-  p.o_res = take(E * sizeof(T));
+  p.o_res = take(s->kind == KIND_ME_RBP ? E * sizeof(T) : 0);
+  p.slotE_bytes = align16(o);
+  // N part
+  o = 0;
   p.o_total = take(N * sizeof(T));
-  p.o_pretot = take(N * sizeof(T));
-  p.o_ci = take(N * sizeof(T));
-  p.rgeo = make_tree((int)E);
-  p.cgeo = make_tree((int)N);
-  const bool rt = s->kind == KIND_RBP || s->kind == KIND_CIRBP || s->kind == KIND_ME_RBP;
-  const bool ct = s->kind == KIND_CIRBP;
-  p.o_rtree = take(rt ? p.rgeo.total * (long long)sizeof(Key) : 0);
-  p.o_ctree = take(ct ? p.cgeo.total * (long long)sizeof(Key) : 0);
-  p.o_mark = 0;
-  p.o_inpp = take(N);
-  const bool me = s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP || s->kind == KIND_ME_RBP;
+  p.o_pretot = take(ci ? N * sizeof(T) : 0);
+  p.o_ci = take(ci ? N * sizeof(T) : 0);
+  p.o_p0t = take(ci ? N * sizeof(T) : 0);
+  p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? N : 0);
   p.o_members = take(me ? std::max(N, np) * 4 : 0);
   p.o_sel = take(me ? np * 4 : 0);
-  p.o_chosen = take(me ? np * 4 : 0);
+  p.o_chosen = take(s->kind == KIND_ME_LMD_CIRBP ? np * 4 : 0);
   p.o_tmp = take(s->kind == KIND_ME_RBP ? np * sizeof(T) : 0);
-  p.slot_bytes = align16(o);
+  p.slotN_bytes = align16(o);
+  // T part
+  o = 0;
+  p.rgeo = make_tree((int)E);
+  p.cgeo = make_tree((int)N);
+  p.flat_ci = N <= kFlatCiMax ? 1 : 0;
+  const bool rt = s->kind == KIND_RBP || s->kind == KIND_CIRBP || s->kind == KIND_ME_RBP;
+  const bool ct = s->kind == KIND_CIRBP && !p.flat_ci;
+  p.o_rtree = take(rt ? p.rgeo.total * (long long)sizeof(Key) : 0);
+  p.o_ridx = take(rt ? p.rgeo.size[1] * 4ll : 0);
+  p.o_ctree = take(ct ? p.cgeo.total * (long long)sizeof(Key) : 0);
+  p.o_cidx = take(ct ? p.cgeo.size[1] * 4ll : 0);
+  p.slotT_bytes = align16(o);
   // per-warp shared scratch
   long long so = 0;
   auto stake = [&](long long bytes) {
@@ -109,8 +129,9 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
     return r;
   };
   const long long dl = std::max<long long>(G->max_items + 2, np + 1);
-  p.so_items = (int)stake((long long)G->max_items * 4);
-  p.so_itemab = (int)stake((long long)G->max_items * 8);
+  p.so_items = (int)stake((long long)G->max_items * 16);
+  p.so_stage = (int)stake(std::max<long long>(((long long)G->max_items + 32) * sizeof(T), 32 * (4 + sizeof(Key))));
+  p.so_nk = (int)stake((long long)G->max_items * sizeof(Key));
   p.so_dl0 = (int)stake(dl * 4);
   p.so_dl1 = (int)stake(dl * 4);
   p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
@@ -118,8 +139,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
 }
 
 template <typename T>
-void* pick_dyn_kernel(int kernel, bool smem) {
-  return sizeof(T) == 8 ? ldpc_dyn_kernel_f64(kernel, smem) : ldpc_dyn_kernel_f32(kernel, smem);
+void* pick_dyn_kernel(int kernel, int mode, int kind) {
+  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind);
 }
 
 template <typename T>
@@ -128,39 +149,68 @@ void* pick_fixed_kernel(int kernel) {
 }
 
 template <typename T>
+int dyn_occupancy(void* fn, int wpb, int smem_bytes) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, wpb * 32, smem_bytes) != cudaSuccess) occ = 0;
+  return occ;
+}
+
+template <typename T>
 int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& pl) {
   memset(&pl, 0, sizeof(pl));
   DynParams& p = pl.p;
   dyn_layout<T>(G, s, p);
-  const int optin = smem_optin() - 1024;
-  const long long per_warp = p.slot_bytes + p.scratch_bytes;
-  pl.smem = !s->force_global && per_warp <= optin;
-  if (pl.smem) {
-    int w = (int)std::min<long long>(8, optin / per_warp);
-    if (per_warp > 56 * 1024) w = 1;  // let several 1-warp CTAs share an SM
-    pl.warps_per_block = std::max(1, w);
-    pl.smem_bytes = (int)(per_warp * pl.warps_per_block);
-  } else {
-    pl.warps_per_block = 8;
-    pl.smem_bytes = p.scratch_bytes * pl.warps_per_block;
+  const long long optin = smem_optin() - 1024;
+  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes, sc = p.scratch_bytes;
+  const long long sh[4] = {sE + sN + sT + sc, sN + sT + sc, sT + sc, sc};
+  const long long hb[4] = {0, sE, sE + sN, sE + sN + sT};
+  struct Cand { int mode, wpb; long long smem; int occ; };
+  auto make = [&](int mode) {
+    Cand c{mode, 0, 0, 0};
+    const long long per = sh[mode];
+    if (per > optin) return c;
+    int w = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / per);
+    c.wpb = std::max(1, w);
+    c.smem = per * c.wpb;
+    c.occ = dyn_occupancy<T>(pick_dyn_kernel<T>(s->kernel, mode, s->kind), c.wpb, (int)c.smem);
+    return c;
+  };
+  Cand cands[4] = {make(0), make(1), make(2), make(3)};
+  auto warps = [](const Cand& c) { return (long long)c.occ * c.wpb; };
+  Cand ch{-1, 0, 0, 0};
+  if (s->placement == 1) ch = cands[3];
+  else if (s->placement == 2) ch = cands[1];
+  else if (s->placement == 3) ch = cands[0];
+  else if (s->placement == 4) ch = cands[2];
+  else {
+    // Most resident frames wins; a mode that keeps more state on chip must
+    // reach at least half the frames of the next one to be preferred.  HBM
+    // parts are kept L2-sized (<= 96 MB) when that is possible.
+    const long long l2 = 96ll << 20;
+    for (int m = 0; m < 4; ++m) {
+      const Cand& c = cands[m];
+      if (c.occ <= 0) continue;
+      const long long frames = std::min<long long>(warps(c) * sm_count(), B);
+      if (ch.mode < 0) { ch = c; continue; }
+      const long long fch = std::min<long long>(warps(ch) * sm_count(), B);
+      const bool l2ok = hb[m] * frames <= l2 || hb[ch.mode] * fch > l2;
+      if (frames >= 2 * fch && l2ok) ch = c;
+    }
   }
-  void* fn = pick_dyn_kernel<T>(s->kernel, pl.smem);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.warps_per_block * 32, pl.smem_bytes) != cudaSuccess || occ < 1)
-    occ = 1;
-  long long blocks = (long long)occ * sm_count();
+  if (ch.mode < 0 || ch.occ <= 0) return LDPC_ERR_UNSUPPORTED;
+  pl.mode = ch.mode;
+  pl.warps_per_block = ch.wpb;
+  pl.smem_bytes = (int)ch.smem;
+  long long blocks = (long long)ch.occ * sm_count();
   long long max_warps = B;
   if (s->max_resident > 0) max_warps = std::min<long long>(max_warps, s->max_resident);
-  if (!pl.smem) {
-    // bound the HBM slot pool to ~24 GB
-    long long cap = std::max<long long>(1, (24ll << 30) / p.slot_bytes);
-    max_warps = std::min(max_warps, cap);
-  }
+  const long long hbm_per_warp = hb[ch.mode];
+  if (hbm_per_warp > 0) max_warps = std::min(max_warps, std::max<long long>(1, (24ll << 30) / hbm_per_warp));
   long long need_blocks = (max_warps + pl.warps_per_block - 1) / pl.warps_per_block;
   blocks = std::max<long long>(1, std::min(blocks, need_blocks));
   pl.blocks = (int)blocks;
-  pl.ws_bytes = 256 + (pl.smem ? 0 : blocks * pl.warps_per_block * p.slot_bytes);
+  pl.ws_bytes = 256 + blocks * pl.warps_per_block * hbm_per_warp;
   return LDPC_OK;
 }
 
@@ -208,6 +258,7 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if (is_dynamic(s->kind) && G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
   if (!is_dynamic(s->kind) && G->max_dc > kFixedMaxDc) return LDPC_ERR_UNSUPPORTED;
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
+  if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
   return LDPC_OK;
 }
 
@@ -221,7 +272,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
   unsigned long long* next = (unsigned long long*)ws;
   if (is_dynamic(s->kind)) {
     DynPlan pl;
-    dyn_plan<T>(G, s, B, pl);
+    if (int rc = dyn_plan<T>(G, s, B, pl)) return rc;
     if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
     if (s->kind == KIND_CIRBP && (!kh || !kt)) return LDPC_ERR_INVALID;
     DynParams& p = pl.p;
@@ -246,9 +297,14 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.kh = kh;
     p.kt = kt;
     p.next = next;
+    p.step_log = g_step_log;
+    p.dbg_full_tree = getenv("LDPC_DEBUG_FULL_TREE") ? 1 : 0;
+    p.dump_step = g_dump_step;
+    p.dump_buf = g_dump_buf;
+    p.log_cap = g_log_cap;
     p.ws = (unsigned char*)ws + 256;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
-    void* fn = pick_dyn_kernel<T>(s->kernel, pl.smem);
+    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind);
     void* args[] = {&p};
     if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,
                                              pl.smem_bytes, st)))
@@ -319,6 +375,19 @@ int ldpc_version(void) { return 10000; }
 
 int ldpc_last_launch_count(void) { return g_last_launches; }
 
+int ldpc_set_state_dump(int64_t step, double* dev_buf) {
+  g_dump_step = step;
+  g_dump_buf = step >= 0 ? dev_buf : nullptr;
+  return LDPC_OK;
+}
+
+int ldpc_set_step_log(int64_t* dev_log, int32_t cap) {
+  if (cap < 0 || (cap > 0 && !dev_log)) return LDPC_ERR_INVALID;
+  g_step_log = cap > 0 ? (long long*)dev_log : nullptr;
+  g_log_cap = cap;
+  return LDPC_OK;
+}
+
 const char* ldpc_strerror(int code) {
   switch (code) {
     case LDPC_OK: return "ok";
@@ -386,11 +455,15 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     for (int m = 0; m < M; ++m) level_checks[fillp[level[m] - 1]++] = m;
   }
   // packed records and per-edge two-hop facts for the dynamic engine
-  std::vector<int> ecv(2ull * E), vrec(2ull * N), vadj(4ull * E), hop_n(E), hop_distinct(E);
+  std::vector<int> ecv(2ull * E), vrec(2ull * N), vadj(4ull * E), erec(4ull * E), hop_n(E), hop_distinct(E);
   std::vector<uint8_t> hop_dup(E, 0);
   for (int e = 0; e < E; ++e) {
     ecv[2 * e] = edge_cn[e];
     ecv[2 * e + 1] = edge_vn[e];
+    erec[4 * e] = edge_cn[e];
+    erec[4 * e + 1] = edge_vn[e];
+    erec[4 * e + 2] = vn_ptr[edge_vn[e]];
+    erec[4 * e + 3] = vn_ptr[edge_vn[e] + 1] - vn_ptr[edge_vn[e]];
   }
   for (int n = 0; n < N; ++n) {
     vrec[2 * n] = vn_ptr[n];
@@ -430,7 +503,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
   // vadj [4E] (16-byte aligned); hop_n [E]; hop_distinct [E]; hop_dup [E bytes]
   size_t base_ints = 3ull * E + (M + 1) + (N + 1) + (n_levels + 1) + M;
   base_ints = (base_ints + 3) & ~size_t(3);
-  size_t total = base_ints + 2ull * E + 2ull * N + 4ull * E + 2ull * E + (E + 3) / 4 + 4;
+  size_t total = base_ints + 2ull * E + 2ull * N + 8ull * E + 2ull * E + (E + 3) / 4 + 8;
   int* d = nullptr;
   if (cudaMalloc(&d, total * sizeof(int)) != cudaSuccess) {
     delete G;
@@ -451,6 +524,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
   size_t oecv = put(ecv.data(), 2ull * E), ovrec = put(vrec.data(), 2ull * N);
   o = (o + 3) & ~size_t(3);
   size_t ovadj = put(vadj.data(), 4ull * E);
+  size_t oerec = put(erec.data(), 4ull * E);
   size_t ohn = put(hop_n.data(), E), ohd = put(hop_distinct.data(), E);
   size_t ohdup = o;
   memcpy(h.data() + o, hop_dup.data(), E);
@@ -481,6 +555,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
   dg.ecv = (const int2*)(d + oecv);
   dg.vrec = (const int2*)(d + ovrec);
   dg.vadj = (const int4*)(d + ovadj);
+  dg.erec = (const int4*)(d + oerec);
   dg.hop_n = d + ohn;
   dg.hop_distinct = d + ohd;
   dg.hop_dup = (const uint8_t*)(d + ohdup);
@@ -514,8 +589,8 @@ int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B,
   if (B > 0) {
     if (is_dynamic(s->kind)) {
       DynPlan pl;
-      if (s->precision == LDPC_F64) dyn_plan<double>(G, s, B, pl);
-      else dyn_plan<float>(G, s, B, pl);
+      int rc = s->precision == LDPC_F64 ? dyn_plan<double>(G, s, B, pl) : dyn_plan<float>(G, s, B, pl);
+      if (rc) return rc;
       ws = pl.ws_bytes;
     } else {
       FixedPlan pl;

@@ -37,6 +37,7 @@ struct DevGraph {
   const int* level_checks;  // [M]
   // packed records for the dynamic engine (one load instead of a dependent chain)
   const int2* ecv;          // [E]  (check, vn) of edge e
+  const int4* erec;         // [E]  (check, vn, vn_ptr[vn], degree of vn) of edge e
   const int2* vrec;         // [N]  (vn_ptr[n], degree of n)
   const int4* vadj;         // [E]  per vn_edges slot k: (f, check i of f, cn_ptr[i], cn_ptr[i+1])
   const int* hop_n;         // [E]  two-hop set size of e (pre-C2V refreshes when e propagates)
@@ -183,6 +184,22 @@ __device__ __forceinline__ unsigned long long warp_max_key_minidx(unsigned long 
 __device__ __forceinline__ unsigned warp_max_key_minidx(unsigned k, int idx, int* idx_out) {
   unsigned m = __reduce_max_sync(kFull, k);
   *idx_out = (int)__reduce_min_sync(kFull, (k == m) ? (unsigned)idx : 0xffffffffu);
+  return m;
+}
+
+// Same over the lanes of `mask` only (disjoint masks may reduce concurrently).
+__device__ __forceinline__ unsigned long long warp_max_key_minidx_masked(unsigned long long k, int idx,
+                                                                         unsigned mask, int* idx_out) {
+  unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  unsigned mh = __reduce_max_sync(mask, hi);
+  unsigned ml = __reduce_max_sync(mask, (hi == mh) ? lo : 0u);
+  *idx_out = (int)__reduce_min_sync(mask, (hi == mh && lo == ml) ? (unsigned)idx : 0xffffffffu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned warp_max_key_minidx_masked(unsigned k, int idx, unsigned mask,
+                                                               int* idx_out) {
+  unsigned m = __reduce_max_sync(mask, k);
+  *idx_out = (int)__reduce_min_sync(mask, (k == m) ? (unsigned)idx : 0xffffffffu);
   return m;
 }
 

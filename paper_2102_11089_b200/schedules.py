@@ -136,14 +136,17 @@ def device_graph(code_or_graph):
 _code_cache = {}
 
 
-def _sched(config: ScheduleConfig, k_info: int, llr_f64: bool, max_resident=0, force_global=False):
+PLACEMENTS = {"auto": 0, "hbm": 1, "split": 2, "smem": 3, "trees": 4}
+
+
+def _sched(config: ScheduleConfig, k_info: int, llr_f64: bool, max_resident=0, placement="auto"):
     seed = int(config.selection_seed) & 0xFFFFFFFFFFFFFFFF
     if seed >= 1 << 63:
         seed -= 1 << 64
     return _native.LdpcSched(KIND_IDS[config.kind], KERNELS[config.kernel], config.i_max,
                              config.n_p, config.n_g, int(k_info), float(config.gamma), seed,
                              PRECISIONS[config.precision], 1 if llr_f64 else 0,
-                             int(max_resident), 1 if force_global else 0)
+                             int(max_resident), PLACEMENTS[placement])
 
 
 def _ptr(t):
@@ -151,7 +154,7 @@ def _ptr(t):
 
 
 def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, device=None,
-                 stream=None, out=None, max_resident=0, force_global=False):
+                 stream=None, out=None, max_resident=0, placement="auto", force_global=False):
     """Decode a batch of frames on the GPU.
 
     code: CodeSpec (k_info taken from it) or TannerGraph (pass k_info).
@@ -159,7 +162,9 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
     Returns a dict of device tensors: u_hat [B,N] int8, prop [B] int64,
     converged [B] bool, counters [B,8] int64, bit_errors_at / info_bit_errors_at
     [B, i_max+1] int32, kappa_hits_iter / kappa_trials_iter [B, i_max] int32.
-    Asynchronous on the current (or given) stream.
+    Asynchronous on the current (or given) stream.  placement (dynamic
+    schedules): "auto", "smem", "split" (per-edge state in HBM/L2, per-VN
+    state in shared memory) or "hbm".
     """
     if isinstance(code, CodeSpec):
         spec = code
@@ -181,7 +186,9 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
         raise ValueError("n_p exceeds the number of variable nodes")
     B = llrs.shape[0]
     I = config.i_max
-    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, force_global)
+    if force_global:
+        placement = "hbm"
+    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, placement)
     if out is None:
         out = {
             "u_hat": torch.empty((B, dg.N), dtype=torch.int8, device=device),
@@ -286,3 +293,22 @@ decode_me_cirbp = _wrap(("me_cirbp",))
 decode_me_lmd_cirbp = _wrap(("me_lmd_cirbp",))
 decode_layered = _wrap(("layered",))
 decode_me_rbp = _wrap(("me_rbp",))
+
+
+def decode_batch_logged(code, llrs, config: ScheduleConfig, log_cap=1000, **kw):
+    """decode_batch plus the propagated edge of each of the first `log_cap`
+    updates per frame ([B, log_cap] int64, -1 past the end) and the committed
+    C2V value (step_c2v, float64) -- debug and near-tie tracing against the
+    CPU oracle's step log."""
+    B = llrs.shape[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    log = torch.full((B, log_cap, 2), -1, dtype=torch.int64, device=dev)
+    L = _native.lib()
+    _native.check(L.ldpc_set_step_log(_ptr(log), int(log_cap)), "ldpc_set_step_log")
+    try:
+        out = decode_batch(code, llrs, config, **kw)
+    finally:
+        L.ldpc_set_step_log(None, 0)
+    out["step_log"] = log[:, :, 0]
+    out["step_c2v"] = log[:, :, 1].view(torch.float64)
+    return out

@@ -6,6 +6,12 @@
   north-star bar: >= 99.9% of frames identical (hard decisions and update
   counts), float64;
 * the two schedules the reference lacks (layered, ME-RBP) against the oracle.
+
+Dynamic schedules: a frame may differ only if its GPU update sequence first
+diverges from the oracle's at a logged near-tie (relative top-2 gap < 1e-5,
+tests/near_tie.py) -- the CUDA and glibc float64 tanh/atanh/exp differ in the
+last ulp, which can only matter at (near-)exact ties.  Fixed schedules
+(flooding, layered) have no argmax and must match exactly.
 """
 
 import numpy as np
@@ -15,6 +21,7 @@ import torch
 from oracle import pyoracle
 from paper_2102_11089_b200.channel import llr_batch
 from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch, results_to_numpy
+from tests.near_tie import trace
 from tests.util import golden_cases, golden_digest_ok, load_code
 
 pytestmark = pytest.mark.gpu
@@ -54,7 +61,17 @@ def test_gpu_matches_reference_golden(fname, code_key, si, sched):
         ok &= (got["kappa_hits_iter"] == z[f"{t}_kh"]).all(1)
         ok &= (got["kappa_trials_iter"] == z[f"{t}_kt"]).all(1)
     bad = np.flatnonzero(~ok)
-    assert len(bad) == 0, f"{sched}: frames {bad.tolist()} differ from the reference"
+    _assert_traced(spec, g, z["llrs"], cfg, bad)
+
+
+def _assert_traced(spec, g, llrs, cfg, bad, limit=24):
+    if len(bad) == 0:
+        return
+    assert cfg.kind not in ("flooding", "layered"), f"{cfg}: frames {bad.tolist()} differ"
+    assert len(bad) <= limit, f"{cfg}: {len(bad)} frames differ"
+    for f, k, gap, ok in trace(spec, g, llrs, cfg, bad):
+        assert ok, (f"{cfg}: frame {f} differs without a near-tie "
+                    f"(first divergent update {k}, oracle gap {gap})")
 
 
 def _compare_oracle(spec, g, llrs, cfg, min_frac=0.999):
@@ -65,6 +82,7 @@ def _compare_oracle(spec, g, llrs, cfg, min_frac=0.999):
     full = same & (got["counters"] == ref["counters"]).all(1) & \
         (got["bit_errors_at"] == ref["bit_errors_at"]).all(1) & (got["converged"] == ref["converged"])
     assert same.mean() >= min_frac, f"{cfg}: {same.mean():.4f} identical"
+    _assert_traced(spec, g, llrs, cfg, np.flatnonzero(~full))
     return same, full
 
 
@@ -98,15 +116,16 @@ def test_minsum_and_new_schedules(kind):
 
 
 @pytest.mark.parametrize("kind", ["rbp", "cirbp", "lmd_cirbp", "flooding"])
-def test_global_state_mode_matches(kind):
-    """HBM-resident frame state (the big-code path) gives the same answers."""
+def test_state_placements_match(kind):
+    """Shared-memory, split and HBM-resident frame state give identical answers."""
     spec, g = load_code("C0")
     llrs = llr_batch(spec, 2.0, seed=0, start=5000, count=300)
     cfg = _cfg({"kind": kind, "i_max": 5})
-    a = _gpu(spec, llrs, cfg)
-    b = _gpu(spec, llrs, cfg, force_global=True)
-    for k in FIELDS:
-        np.testing.assert_array_equal(a[k], b[k])
+    a = _gpu(spec, llrs, cfg, placement="smem")
+    for pl in ("split", "hbm"):
+        b = _gpu(spec, llrs, cfg, placement=pl)
+        for k in FIELDS:
+            np.testing.assert_array_equal(a[k], b[k])
 
 
 def test_small_batches_and_imax0():

@@ -23,10 +23,13 @@ for key in codes:
     eb = {"C0": 2.0, "C1": 2.0, "C2": 1.0, "C3": 1.0}[key]
     llr = llr_batch(spec, eb, 0, 0, nfr)
     for kind in kinds:
-        for fg in (False, True):
+        for fg in ("auto", "smem", "split", "trees", "hbm"):
             cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=4)
             t = time.time()
-            out = decode_batch(spec, torch.from_numpy(llr).cuda(), cfg, force_global=fg)
+            try:
+                out = decode_batch(spec, torch.from_numpy(llr).cuda(), cfg, placement=fg)
+            except RuntimeError as ex:
+                print(key, kind, fg, 'skipped:', ex); continue
             torch.cuda.synchronize()
             dt = time.time() - t
             got = results_to_numpy(out, kind, imax)
@@ -34,7 +37,7 @@ for key in codes:
             same = (got["u_hat"] == ref["u_hat"]).all(1) & (got["prop"] == ref["prop"])
             cnt = (got["counters"] == ref["counters"]).all(1)
             be = (got["bit_errors_at"] == ref["bit_errors_at"]).all(1)
-            print(f"{key} {kind:13s} global={int(fg)} same={same.mean():.4f} counters={cnt.mean():.4f} "
+            print(f"{key} {kind:13s} {fg:5s} same={same.mean():.4f} counters={cnt.mean():.4f} "
                   f"biterr={be.mean():.4f} conv={np.mean(got['converged'] == ref['converged']):.4f} "
                   f"gpu {dt*1e3:.1f} ms", flush=True)
             if not same.all():

@@ -17,7 +17,7 @@ from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch  # noqa
 
 key, kind, nfr = sys.argv[1], sys.argv[2], int(sys.argv[3])
 flags = sys.argv[4:]
-fg = "global" in flags
+placement = next((f for f in flags if f in ("smem", "split", "hbm", "trees")), "hbm" if "global" in flags else "auto")
 prec = "f32" if "f32" in flags else "f64"
 n_p = 4
 for f in flags:
@@ -30,12 +30,12 @@ if key == "C4":
     spec = configs.make_c2_code()
 llr = torch.from_numpy(llr_batch(spec, eb, 0, 0, nfr)).cuda()
 cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=n_p, precision=prec)
-decode_batch(spec, llr[:1], cfg, force_global=fg)
+decode_batch(spec, llr[:1], cfg, placement=placement)
 torch.cuda.synchronize()
 t = time.time()
-out = decode_batch(spec, llr, cfg, force_global=fg)
+out = decode_batch(spec, llr, cfg, placement=placement)
 torch.cuda.synchronize()
 dt = time.time() - t
 upd = int(out["counters"][:, 0].sum())
-print(f"{key} {kind} {prec} global={fg} frames={nfr} time={dt*1e3:.2f} ms updates={upd} "
+print(f"{key} {kind} {prec} {placement} frames={nfr} time={dt*1e3:.2f} ms updates={upd} "
       f"upd/s={upd/dt:.3e} frames/s={nfr/dt:.3e} us/update/warp-est={dt*1e6/max(1,upd/nfr):.2f}")
