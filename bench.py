@@ -211,6 +211,10 @@ def run_ours(args, wl):
     key, ebn0, i_max, batch, scheds = wl
     if args.batch:
         batch = args.batch
+    if args.only:
+        scheds = [s for s in scheds if s[0] + (f"/M{s[1]}" if s[0].startswith("me_") else "") == args.only]
+        if not scheds:
+            raise SystemExit(f"--only {args.only}: not a schedule of {key}")
     spec = getattr(configs, f"make_{key.lower()}_code")()
     g = build_tanner(spec.h)
     dg = device_graph(g)
@@ -301,6 +305,15 @@ def run_ours(args, wl):
     achieved = w["updates"] * w["bpu"] / (sched_ms[dom] / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # DRAM traffic of this kernel from a committed ncu --set full capture of
+    # `bench.py --only <kernel>` (profiles/traffic.json), per launch
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    dom_name = cfgs[dom].kind + (f"/M{cfgs[dom].n_p}" if cfgs[dom].kind.startswith("me_") else "")
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(f"{key}:{dom_name}:{args.precision}:{batch}")
+        traffic = t.get("dram_bytes_per_launch") if t else None
     per = {}
     for i, (c, wk) in enumerate(zip(cfgs, work)):
         nm = c.kind + (f"/M{c.n_p}" if c.kind.startswith("me_") else "")
@@ -320,10 +333,12 @@ def run_ours(args, wl):
                    "parallelism": f"frames sharded over {world} GPU(s)"},
         "per_schedule": per,
         "roofline": {"bound": "hbm", "kernel": list(per)[dom], "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                     "note": "algorithmic message-state bytes (SURVEY 8(d) formula, %s) / kernel time; "
-                             "state is SMEM-resident for this code, so HBM peak is the stated "
-                             "denominator of measured" % args.precision},
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "note": "achieved = algorithmic message-state bytes per launch (SURVEY 8(d) "
+                             "formula in %s units x the launch's C2V updates) / the launch's CUDA-event "
+                             "time; the dynamic schedules are a serial update chain per frame "
+                             "(latency-bound), so this fraction is low by construction" % args.precision},
         "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,
@@ -350,6 +365,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--only", default="", help="run one schedule of the workload (e.g. cirbp, me_rbp/M4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT"):
         args.warmup = 3

@@ -184,18 +184,18 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
   else if (s->placement == 3) ch = cands[0];
   else if (s->placement == 4) ch = cands[2];
   else {
-    // Most resident frames wins; a mode that keeps more state on chip must
-    // reach at least half the frames of the next one to be preferred.  HBM
-    // parts are kept L2-sized (<= 96 MB) when that is possible.
-    const long long l2 = 96ll << 20;
-    for (int m = 0; m < 4; ++m) {
+    // The update chain is latency-bound, so resident frames decide throughput
+    // (measured on C0-C2: split/trees placements with 16-24 warps/SM beat the
+    // all-shared 3-5 warps/SM by ~2x even when the per-edge part spills past
+    // L2).  Most resident frames wins; within 10% the more on-chip mode wins.
+    long long best = 0;
+    for (int m = 0; m < 4; ++m)
+      if (cands[m].occ > 0) best = std::max(best, std::min<long long>(warps(cands[m]) * sm_count(), B));
+    for (int m = 0; m < 4 && ch.mode < 0; ++m) {
       const Cand& c = cands[m];
       if (c.occ <= 0) continue;
       const long long frames = std::min<long long>(warps(c) * sm_count(), B);
-      if (ch.mode < 0) { ch = c; continue; }
-      const long long fch = std::min<long long>(warps(ch) * sm_count(), B);
-      const bool l2ok = hb[m] * frames <= l2 || hb[ch.mode] * fch > l2;
-      if (frames >= 2 * fch && l2ok) ch = c;
+      if (frames * 10 >= best * 9) ch = c;
     }
   }
   if (ch.mode < 0 || ch.occ <= 0) return LDPC_ERR_UNSUPPORTED;
