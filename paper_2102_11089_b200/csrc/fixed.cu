@@ -2,7 +2,13 @@
 #include "fixed_engine.cuh"
 #include "kernel_table.h"
 using namespace ldpc;
-void* ldpc_fixed_kernel(int f64, int kernel) {
-  if (f64) return kernel == KERNEL_EXACT ? (void*)fixed_decode_kernel<double, KERNEL_EXACT> : (void*)fixed_decode_kernel<double, KERNEL_MINSUM>;
-  return kernel == KERNEL_EXACT ? (void*)fixed_decode_kernel<float, KERNEL_EXACT> : (void*)fixed_decode_kernel<float, KERNEL_MINSUM>;
+void* ldpc_fixed_kernel(int f64, int kernel, int layered) {
+  if (f64) {
+    if (kernel == KERNEL_EXACT)
+      return layered ? (void*)fixed_decode_kernel<double, KERNEL_EXACT, true> : (void*)fixed_decode_kernel<double, KERNEL_EXACT, false>;
+    return layered ? (void*)fixed_decode_kernel<double, KERNEL_MINSUM, true> : (void*)fixed_decode_kernel<double, KERNEL_MINSUM, false>;
+  }
+  if (kernel == KERNEL_EXACT)
+    return layered ? (void*)fixed_decode_kernel<float, KERNEL_EXACT, true> : (void*)fixed_decode_kernel<float, KERNEL_EXACT, false>;
+  return layered ? (void*)fixed_decode_kernel<float, KERNEL_MINSUM, true> : (void*)fixed_decode_kernel<float, KERNEL_MINSUM, false>;
 }

@@ -1,4 +1,4 @@
-// fixed_engine.cuh -- flooding and row-layered BP, frame-interleaved.
+// fixed_engine.cuh -- flooding and row-layered BP, frame-interleaved, tiled.
 //
 // Flooding replaces _decode_flooding (E:719-765): per iteration all C2V from
 // the previous V2C, then totals and V2C per VN, syndrome at every iteration.
@@ -7,20 +7,34 @@
 // total += c2v' - c2v.  Checks are grouped into dependency levels on the host
 // (a check's level exceeds that of every earlier check sharing a VN), so a
 // level runs in parallel and still reproduces the sequential order exactly.
+// Flooding is the one-level case (all checks read the previous totals).
 //
-// Layout: a CTA owns a group of F frames; its state arrays are interleaved
-// [item][F] so consecutive lanes are consecutive frames and every message
-// access is a coalesced 32 x 8 B row.  Only c2v[E] and total[N] are kept: the
-// V2C of an edge is clamp(total - c2v) (bit-identical to the reference's
-// stored v2c, E:752-754), so per edge update the traffic is c2v read+write,
-// one total gather and the VN-phase re-read -- the 16 + 8N/E B roofline figure
-// (in float32 units; double for float64).
+// Layout: a CTA owns a group of 32 frames; its HBM slot holds chl[N][32],
+// total[N][32], c2v[E][32] (frame index fastest, so one warp = 32 frames moves
+// one coalesced 256-byte row per access) and sign[N] words.  Only c2v and
+// totals are kept: the V2C of an edge is clamp(total - c2v), bit-identical to
+// the reference's stored v2c (E:752-754).
+//
+// Each level is cut (on the host) into tiles of <= kTileEdges edges made of
+// whole checks.  Per tile, phase A spreads the tile's edges over all warps:
+// gather the c2v row and the total row, form in = tanh(clamp(total - c2v)/2)
+// (or v2c for min-sum) into shared memory; phase B gives every (edge, frame)
+// a thread: the exact left-to-right product of its check's other inputs from
+// shared memory, atanh, store (layered also commits total += new - old).  No
+// per-thread arrays, so registers stay low and many warps keep many 256-byte
+// rows in flight -- the kernel is HBM-bound on large codes.
+//
+// Syndrome / bit errors: the VN pass writes each VN's 32 frame sign bits as
+// one word (warp ballot) to the L2-resident sign[] array and tallies errors
+// per lane; a check's parity for 32 frames is the XOR of its VNs' words.
 #pragma once
 #include "ldpc_common.cuh"
 
 namespace ldpc {
 
 constexpr int kFixedMaxDc = 32;
+constexpr int kFixedFrames = 32;  // frames per CTA (= warp lanes)
+constexpr int kTileEdges = 128;   // edges per shared-memory tile
 
 struct FixedParams {
   DevGraph g;
@@ -35,109 +49,166 @@ struct FixedParams {
   int* biterr;
   int* biterr_info;
   unsigned long long* next;
-  unsigned char* ws;      // per-CTA slot: chl[N][F], total[N][F], c2v[E][F]
+  unsigned char* ws;      // per-CTA slot: chl[N][32], total[N][32], c2v[E][32], sign[N]
   long long slot_bytes;
-  int F;                  // frames per CTA (power of two, <= 32)
-  int log2F;
+  // tiling of the schedule (flooding: one level in check order; layered: levels)
+  int n_levels;
+  const int* level_tptr;  // [n_levels+1] tile range of each level
+  const int* tile_eptr;   // [n_tiles+1] offsets into te_list
+  const int* te_list;     // [E] global edge id, tile order
+  const int2* te_chk;     // [E] tile-local [a, b) of the edge's check
+  const int* tile_cptr;   // [n_tiles+1] offsets into tc_rec
+  const int4* tc_rec;     // [M] per check in tile order: (local a, degree, first edge id, 0)
 };
 
-// C2V of one check for one frame: inputs from total/c2v, outputs written back.
-// LAYERED additionally commits total += new - old per edge.
-template <typename T, int KERNEL, bool LAYERED>
-__device__ __forceinline__ void check_update(const DevGraph& g, int m, int F, int fl, T* c2v, T* total) {
-  const int a = g.cn_ptr[m], d = g.cn_ptr[m + 1] - a;
-  T in[kFixedMaxDc];
-#pragma unroll 4
-  for (int q = 0; q < d; ++q) {
-    int e = a + q;
-    T v = clampv(total[(long long)g.edge_vn[e] * F + fl] - c2v[(long long)e * F + fl]);
-    in[q] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;  // E:58 / E:73
-  }
-  for (int q = 0; q < d; ++q) {
-    T out;
-    if (KERNEL == KERNEL_EXACT) {
-      T prod = T(1);
-      for (int r = 0; r < d; ++r)
-        if (r != q) prod *= in[r];
-      out = atanh_msg(prod, d - 1);
-    } else {
-      T sign = T(1), mag = Num<T>::kBig;
-      for (int r = 0; r < d; ++r) {
-        if (r == q) continue;
-        T v = in[r];
-        if (v < T(0)) { sign = -sign; v = -v; }
-        if (v < mag) mag = v;
-      }
-      out = d > 1 ? clampv(sign * mag) : T(0);
+template <typename T, int KERNEL>
+__device__ __forceinline__ T tile_out(const T* in_s, int2 ck, int el, int lane) {
+  if (KERNEL == KERNEL_EXACT) {
+    T prod = T(1);
+    for (int q = ck.x; q < ck.y; ++q)
+      if (q != el) prod *= in_s[q * kFixedFrames + lane];
+    return atanh_msg(prod, ck.y - ck.x - 1);
+  } else {
+    T sign = T(1), mag = Num<T>::kBig;
+    for (int q = ck.x; q < ck.y; ++q) {
+      if (q == el) continue;
+      T v = in_s[q * kFixedFrames + lane];
+      if (v < T(0)) { sign = -sign; v = -v; }
+      if (v < mag) mag = v;
     }
-    long long ix = (long long)(a + q) * F + fl;
-    if (LAYERED) {
-      long long tx = (long long)g.edge_vn[a + q] * F + fl;
-      total[tx] += out - c2v[ix];
-    }
-    c2v[ix] = out;
+    return ck.y - ck.x > 1 ? clampv(sign * mag) : T(0);
   }
 }
 
-template <typename T, int KERNEL>
+constexpr int kPhaseBRegs = 16;  // checks up to this degree keep their inputs in registers
+
+// All C2V outputs of one check for one frame (lane), inputs from the tile in
+// shared memory.  Exact kernel: prod_q = prefix(in_0..in_{q-1}) continued by
+// in_{q+1}..in_{d-1} -- the reference's left-to-right product (E:55-59) with
+// the prefix shared across outputs.
+template <typename T, int KERNEL, bool LAYERED>
+__device__ __forceinline__ void check_outputs(const DevGraph& g, const T* in_s, const T* old_s, int4 rec,
+                                              int lane, bool act, T* c2v, T* total) {
+  constexpr int F = kFixedFrames;
+  const int la = rec.x, d = rec.y, ga = rec.z;
+  if (d <= kPhaseBRegs) {
+    T in[kPhaseBRegs];
+#pragma unroll
+    for (int q = 0; q < kPhaseBRegs; ++q)
+      if (q < d) in[q] = in_s[(la + q) * F + lane];
+    T pre = T(1);
+#pragma unroll
+    for (int q = 0; q < kPhaseBRegs; ++q) {
+      if (q >= d) break;
+      T out;
+      if (KERNEL == KERNEL_EXACT) {
+        T prod = pre;
+#pragma unroll
+        for (int r = q + 1; r < kPhaseBRegs; ++r)
+          if (r < d) prod *= in[r];
+        out = atanh_msg(prod, d - 1);
+        pre *= in[q];
+      } else {
+        T sign = T(1), mag = Num<T>::kBig;
+#pragma unroll
+        for (int r = 0; r < kPhaseBRegs; ++r) {
+          if (r >= d || r == q) continue;
+          T v = in[r];
+          if (v < T(0)) { sign = -sign; v = -v; }
+          if (v < mag) mag = v;
+        }
+        out = d > 1 ? clampv(sign * mag) : T(0);
+      }
+      if (act) {
+        c2v[(long long)(ga + q) * F + lane] = out;
+        if (LAYERED) total[(long long)g.edge_vn[ga + q] * F + lane] += out - old_s[(la + q) * F + lane];
+      }
+    }
+  } else {
+    for (int q = 0; q < d; ++q) {
+      const T out = tile_out<T, KERNEL>(in_s, make_int2(la, la + d), la + q, lane);
+      if (act) {
+        c2v[(long long)(ga + q) * F + lane] = out;
+        if (LAYERED) total[(long long)g.edge_vn[ga + q] * F + lane] += out - old_s[(la + q) * F + lane];
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void sign_row(int n, T tv, int k_info, unsigned* sign, int lane, int& errs,
+                                         int& errs_info) {
+  const bool neg = tv < T(0);
+  const unsigned w = __ballot_sync(kFull, neg);
+  if (lane == 0) sign[n] = w;
+  if (neg) {
+    ++errs;
+    if (n < k_info) ++errs_info;
+  }
+}
+
+template <typename T, int KERNEL, bool LAYERED>
 __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant__ FixedParams p) {
   const DevGraph& g = p.g;
-  const int F = p.F, lf = p.log2F, tid = threadIdx.x, nt = blockDim.x;
-  const int fl = tid & (F - 1), slot_item0 = tid >> lf, items_per_pass = nt >> lf;
+  constexpr int F = kFixedFrames;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int I = p.i_max;
-  const bool layered = p.kind == KIND_LAYERED;
   T* chl = (T*)(p.ws + (long long)blockIdx.x * p.slot_bytes);
   T* total = chl + (long long)g.N * F;
   T* c2v = total + (long long)g.N * F;
-  __shared__ int s_active[32], s_unsat[32], s_errs[32], s_errs_info[32], s_iter[32];
+  unsigned* sign = (unsigned*)(c2v + (long long)g.E * F);
+  extern __shared__ __align__(16) unsigned char fixed_smem[];
+  T* in_s = (T*)fixed_smem;            // [kTileEdges][32]
+  T* old_s = in_s + kTileEdges * F;    // [kTileEdges][32], layered only
+  __shared__ int s_active[F], s_errs[F], s_errs_info[F], s_iter[F];
+  __shared__ unsigned s_unsat;
   __shared__ unsigned long long s_grp;
   for (;;) {
     if (tid == 0) s_grp = atomicAdd(p.next, 1ull);
     __syncthreads();
     const long long f0 = (long long)s_grp * F;
     if (f0 >= p.B) break;
-    // load channel LLRs, c2v = 0, total = chl
-    for (long long x = tid; x < (long long)g.N * F; x += nt) {
-      int n = (int)(x >> lf), q = (int)(x & (F - 1));
-      long long f = f0 + q;
-      T v = T(0);
-      if (f < p.B) v = p.llr_f64 ? (T)((const double*)p.llr)[f * g.N + n] : (T)((const float*)p.llr)[f * g.N + n];
-      chl[x] = v;
-      total[x] = v;
-    }
-    for (long long x = tid; x < (long long)g.E * F; x += nt) c2v[x] = T(0);
+    const long long fl_glob = f0 + lane;
+    const bool lane_valid = fl_glob < p.B;
     if (tid < F) {
       s_active[tid] = (f0 + tid) < p.B;
       s_iter[tid] = 0;
+      s_errs[tid] = s_errs_info[tid] = 0;
     }
+    if (tid == 0) s_unsat = 0;
+    // load LLRs (transposed into [N][32]), c2v = 0, total = chl; boundary-0 tallies
+    int errs = 0, errs_info = 0;
+    for (int n = warp; n < g.N; n += nw) {
+      T v = T(0);
+      if (lane_valid)
+        v = p.llr_f64 ? (T)((const double*)p.llr)[fl_glob * g.N + n] : (T)((const float*)p.llr)[fl_glob * g.N + n];
+      chl[(long long)n * F + lane] = v;
+      total[(long long)n * F + lane] = v;
+      sign_row<T>(n, v, p.k_info, sign, lane, errs, errs_info);
+    }
+    for (long long x = tid; x < (long long)g.E * F; x += nt) c2v[x] = T(0);
+    __syncthreads();
+    atomicAdd(&s_errs[lane], errs);
+    atomicAdd(&s_errs_info[lane], errs_info);
     __syncthreads();
     for (int it = 0;; ++it) {
-      // record boundary `it` + syndrome for active frames
-      if (tid < F) { s_errs[tid] = 0; s_errs_info[tid] = 0; s_unsat[tid] = 0; }
-      __syncthreads();
-      for (long long x = tid; x < (long long)g.N * F; x += nt) {
-        int n = (int)(x >> lf), q = (int)(x & (F - 1));
-        if (s_active[q] && total[x] < T(0)) {
-          atomicAdd(&s_errs[q], 1);
-          if (n < p.k_info) atomicAdd(&s_errs_info[q], 1);
+      if (it > 0) {  // boundary `it`: syndrome from the sign words, 32 frames per check
+        unsigned bad = 0;
+        for (int m = tid; m < g.M; m += nt) {
+          unsigned par = 0;
+          for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e) par ^= sign[g.edge_vn[e]];
+          bad |= par;
         }
+        bad = __reduce_or_sync(kFull, bad);
+        if (lane == 0 && bad) atomicOr(&s_unsat, bad);
       }
-      if (it > 0)
-        for (long long x = tid; x < (long long)g.M * F; x += nt) {
-          int m = (int)(x >> lf), q = (int)(x & (F - 1));
-          if (!s_active[q]) continue;
-          int par = 0;
-          for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e)
-            par ^= total[(long long)g.edge_vn[e] * F + q] < T(0) ? 1 : 0;
-          if (par) s_unsat[q] = 1;
-        }
       __syncthreads();
       if (tid < F && s_active[tid]) {
-        long long f = f0 + tid;
+        const long long f = f0 + tid;
         p.biterr[f * (I + 1) + it] = s_errs[tid];
         p.biterr_info[f * (I + 1) + it] = s_errs_info[tid];
         bool done = false;
-        if (it > 0 && !s_unsat[tid]) {  // converged at iteration it (E:761-764)
+        if (it > 0 && !((s_unsat >> tid) & 1u)) {  // converged at iteration it (E:761-764)
           done = true;
           p.conv[f] = 1;
           for (int kk = it + 1; kk <= I; ++kk) {
@@ -154,69 +225,111 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
         }
       }
       __syncthreads();
-      int any = 0;
+      unsigned any = 0;
       for (int q = 0; q < F; ++q) any |= s_active[q];
       if (!any) break;
-      // one iteration
-      if (!layered) {
-        for (int m0 = 0; m0 < g.M; m0 += items_per_pass) {
-          int m = m0 + slot_item0;
-          if (m < g.M && s_active[fl]) check_update<T, KERNEL, false>(g, m, F, fl, c2v, total);
-        }
-        __syncthreads();
-        for (int n0 = 0; n0 < g.N; n0 += items_per_pass) {
-          int n = n0 + slot_item0;
-          if (n < g.N && s_active[fl]) {
-            long long nx = (long long)n * F + fl;
-            T s = chl[nx];
-            for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) s += c2v[(long long)g.vn_edges[k] * F + fl];
-            total[nx] = s;
+      const bool act = s_active[lane] != 0;
+      __syncthreads();
+      if (tid < F) s_errs[tid] = s_errs_info[tid] = 0;
+      if (tid == 0) s_unsat = 0;
+      // ---- check phase, tile by tile, level by level
+      for (int L = 0; L < p.n_levels; ++L) {
+        for (int t = p.level_tptr[L]; t < p.level_tptr[L + 1]; ++t) {
+          const int ea = p.tile_eptr[t], ne = p.tile_eptr[t + 1] - ea;
+          // phase A: 4 edges per warp in flight (loads first, then the math)
+          for (int el0 = warp; el0 < ne; el0 += 4 * nw) {
+            T o[4], tv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int el = el0 + u * nw;
+              if (el < ne) {
+                const int e = p.te_list[ea + el];
+                o[u] = c2v[(long long)e * F + lane];
+                tv[u] = total[(long long)g.edge_vn[e] * F + lane];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int el = el0 + u * nw;
+              if (el < ne) {
+                const T v = clampv(tv[u] - o[u]);
+                in_s[el * F + lane] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;  // E:58 / E:73
+                if (LAYERED) old_s[el * F + lane] = o[u];
+              }
+            }
           }
-        }
-        __syncthreads();
-      } else {
-        for (int L = 0; L < g.n_levels; ++L) {
-          int a = g.level_ptr[L], b = g.level_ptr[L + 1];
-          for (int k0 = a; k0 < b; k0 += items_per_pass) {
-            int k = k0 + slot_item0;
-            if (k < b && s_active[fl]) check_update<T, KERNEL, true>(g, g.level_checks[k], F, fl, c2v, total);
+          __syncthreads();
+          if (sizeof(T) == 4) {
+            // phase B (float32): one warp per check, inputs in registers, shared prefix
+            for (int ck = p.tile_cptr[t] + warp; ck < p.tile_cptr[t + 1]; ck += nw)
+              check_outputs<T, KERNEL, LAYERED>(g, in_s, old_s, p.tc_rec[ck], lane, act, c2v, total);
+          } else {
+            // phase B (float64): one warp per edge -- register-light, so twice the warps
+            for (int el = warp; el < ne; el += nw) {
+              const int e = p.te_list[ea + el];
+              const T out = tile_out<T, KERNEL>(in_s, p.te_chk[ea + el], el, lane);
+              if (act) {
+                c2v[(long long)e * F + lane] = out;
+                if (LAYERED) total[(long long)g.edge_vn[e] * F + lane] += out - old_s[el * F + lane];
+              }
+            }
           }
           __syncthreads();
         }
       }
+      // ---- VN pass: totals (flooding), sign words, error tallies
+      errs = errs_info = 0;
+      for (int n = warp; n < g.N; n += nw) {
+        const long long nx = (long long)n * F + lane;
+        T s;
+        if (!LAYERED && act) {
+          s = chl[nx];
+          const int k0 = g.vn_ptr[n], k1 = g.vn_ptr[n + 1];
+          for (int k = k0; k < k1; k += 4) {  // 4 rows in flight, summed in order (E:749-750)
+            T r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k + u < k1) r[u] = c2v[(long long)g.vn_edges[k + u] * F + lane];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k + u < k1) s += r[u];
+          }
+          total[nx] = s;
+        } else {
+          s = total[nx];
+        }
+        sign_row<T>(n, s, p.k_info, sign, lane, errs, errs_info);
+      }
+      if (act) {
+        atomicAdd(&s_errs[lane], errs);
+        atomicAdd(&s_errs_info[lane], errs_info);
+      }
+      __syncthreads();
     }
     // outputs
-    for (long long x = tid; x < (long long)g.N * F; x += nt) {
-      int n = (int)(x >> lf), q = (int)(x & (F - 1));
-      long long f = f0 + q;
-      if (f < p.B) p.u_hat[f * g.N + n] = total[x] < T(0) ? 1 : 0;
-    }
+    for (int n = warp; n < g.N; n += nw)
+      if (lane_valid) p.u_hat[fl_glob * g.N + n] = (sign[n] >> lane) & 1u;
     if (tid < F && f0 + tid < p.B) {
-      long long f = f0 + tid;
-      long long prop = (long long)s_iter[tid] * g.E;
-      if (I == 0) {
-        prop = 0;
-        // converged = syndrome of the channel decisions (schedules.py:144-146)
-        p.conv[f] = 0;
-      }
+      const long long f = f0 + tid;
+      const long long prop = I == 0 ? 0 : (long long)s_iter[tid] * g.E;
       p.prop[f] = prop;
       p.counters[f * kCounters + C_PROP] = prop;
       p.counters[f * kCounters + C_V2C] = prop;
       for (int k = 2; k < kCounters; ++k) p.counters[f * kCounters + k] = 0;
     }
-    if (I == 0) {
-      // syndrome of channel decisions
-      if (tid < F) s_unsat[tid] = 0;
+    if (I == 0) {  // converged = syndrome of the channel decisions (schedules.py:144-146)
+      if (tid == 0) s_unsat = 0;
       __syncthreads();
-      for (long long x = tid; x < (long long)g.M * F; x += nt) {
-        int m = (int)(x >> lf), q = (int)(x & (F - 1));
-        int par = 0;
-        for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e)
-          par ^= total[(long long)g.edge_vn[e] * F + q] < T(0) ? 1 : 0;
-        if (par) s_unsat[q] = 1;
+      unsigned bad = 0;
+      for (int m = tid; m < g.M; m += nt) {
+        unsigned par = 0;
+        for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e) par ^= sign[g.edge_vn[e]];
+        bad |= par;
       }
+      bad = __reduce_or_sync(kFull, bad);
+      if (lane == 0 && bad) atomicOr(&s_unsat, bad);
       __syncthreads();
-      if (tid < F && f0 + tid < p.B) p.conv[f0 + tid] = s_unsat[tid] ? 0 : 1;
+      if (tid < F && f0 + tid < p.B) p.conv[f0 + tid] = ((s_unsat >> tid) & 1u) ? 0 : 1;
     }
     __syncthreads();
   }

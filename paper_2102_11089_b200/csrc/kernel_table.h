@@ -22,4 +22,4 @@ inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind) {
     default: return dyn_f64_exact_d_get(mode, kind);
   }
 }
-void* ldpc_fixed_kernel(int f64, int kernel);
+void* ldpc_fixed_kernel(int f64, int kernel, int layered);

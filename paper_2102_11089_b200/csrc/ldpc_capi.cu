@@ -15,10 +15,22 @@
 
 using namespace ldpc;
 
+struct Tiling {  // fixed-engine schedule tiling (see fixed_engine.cuh)
+  int n_levels;
+  int* level_tptr;
+  int* tile_eptr;
+  int* te_list;
+  int2* te_chk;
+  int* tile_cptr;
+  int4* tc_rec;
+};
+
 struct ldpc_graph {
   DevGraph d;
   int* dev_block;  // one allocation for every device array
   int max_dv, max_dc, max_items;
+  Tiling flood, layer;
+  int* tile_block;
 };
 
 namespace {
@@ -144,8 +156,8 @@ void* pick_dyn_kernel(int kernel, int mode, int kind) {
 }
 
 template <typename T>
-void* pick_fixed_kernel(int kernel) {
-  return ldpc_fixed_kernel(sizeof(T) == 8, kernel);
+void* pick_fixed_kernel(int kernel, int layered) {
+  return ldpc_fixed_kernel(sizeof(T) == 8, kernel, layered);
 }
 
 template <typename T>
@@ -218,23 +230,22 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
 
 struct FixedPlan {
   FixedParams p;
-  int threads, blocks;
+  int threads, blocks, smem_bytes;
   long long ws_bytes;
 };
 
 template <typename T>
 int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPlan& pl) {
   memset(&pl, 0, sizeof(pl));
-  int F = 32;
-  while (F > 1 && F / 2 >= B) F /= 2;
-  pl.p.F = F;
-  pl.p.log2F = 0;
-  while ((1 << pl.p.log2F) < F) ++pl.p.log2F;
-  pl.p.slot_bytes = align16((2ll * G->d.N + G->d.E) * F * sizeof(T));
-  pl.threads = 256;
-  void* fn = pick_fixed_kernel<T>(s->kernel);
+  const int F = kFixedFrames;
+  const bool layered = s->kind == KIND_LAYERED;
+  pl.p.slot_bytes = align16((2ll * G->d.N + G->d.E) * F * sizeof(T) + 4ll * G->d.N);
+  pl.threads = 512;
+  pl.smem_bytes = (layered ? 2 : 1) * kTileEdges * F * (int)sizeof(T);
+  void* fn = pick_fixed_kernel<T>(s->kernel, layered);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.threads, pl.smem_bytes) != cudaSuccess || occ < 1) occ = 1;
   long long groups = (B + F - 1) / F;
   long long blocks = std::min<long long>((long long)occ * sm_count(), groups);
   if (s->max_resident > 0) blocks = std::min<long long>(blocks, std::max(1, s->max_resident / F));
@@ -242,6 +253,14 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
   blocks = std::max<long long>(1, std::min(blocks, cap));
   pl.blocks = (int)blocks;
   pl.ws_bytes = 256 + blocks * pl.p.slot_bytes;
+  const Tiling& tl = layered ? G->layer : G->flood;
+  pl.p.n_levels = tl.n_levels;
+  pl.p.level_tptr = tl.level_tptr;
+  pl.p.tile_eptr = tl.tile_eptr;
+  pl.p.te_list = tl.te_list;
+  pl.p.te_chk = tl.te_chk;
+  pl.p.tile_cptr = tl.tile_cptr;
+  pl.p.tc_rec = tl.tc_rec;
   return LDPC_OK;
 }
 
@@ -256,7 +275,7 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if ((s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && s->n_p > G->d.N)
     return LDPC_ERR_INVALID;  // schedules.py:136-137
   if (is_dynamic(s->kind) && G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
-  if (!is_dynamic(s->kind) && G->max_dc > kFixedMaxDc) return LDPC_ERR_UNSUPPORTED;
+  if (!is_dynamic(s->kind) && G->max_dc > kTileEdges) return LDPC_ERR_UNSUPPORTED;
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
   if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
   return LDPC_OK;
@@ -312,7 +331,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     g_last_launches = 1;
   } else {
     FixedPlan pl;
-    fixed_plan<T>(G, s, B, pl);
+    if (int rc = fixed_plan<T>(G, s, B, pl)) return rc;
     if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
     FixedParams& p = pl.p;
     p.g = G->d;
@@ -333,9 +352,9 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.ws = (unsigned char*)ws + 256;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
     if (int rc = cuda_check(cudaMemsetAsync(conv, 0, B, st))) return rc;
-    void* fn = pick_fixed_kernel<T>(s->kernel);
+    void* fn = pick_fixed_kernel<T>(s->kernel, s->kind == KIND_LAYERED);
     void* args[] = {&p};
-    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.threads), args, 0, st)))
+    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.threads), args, pl.smem_bytes, st)))
       return rc;
     g_last_launches = 1;
   }
@@ -454,6 +473,44 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     std::vector<int> fillp(level_ptr.begin(), level_ptr.end() - 1);
     for (int m = 0; m < M; ++m) level_checks[fillp[level[m] - 1]++] = m;
   }
+  // fixed-engine tilings: per level, whole checks packed into tiles of <= kTileEdges edges
+  struct HostTiling {
+    std::vector<int> level_tptr, tile_eptr, te_list, te_chk, tile_cptr, tc_rec;
+  } ht[2];
+  auto build_tiling = [&](HostTiling& t, const std::vector<int>& lvl_ptr, const std::vector<int>& chk) {
+    t.level_tptr.push_back(0);
+    t.tile_eptr.push_back(0);
+    t.tile_cptr.push_back(0);
+    for (size_t L = 0; L + 1 < lvl_ptr.size(); ++L) {
+      int cur = 0;
+      for (int k = lvl_ptr[L]; k < lvl_ptr[L + 1]; ++k) {
+        const int m = chk[k], d = cn_ptr[m + 1] - cn_ptr[m];
+        if (cur > 0 && cur + d > kTileEdges) {
+          t.tile_eptr.push_back((int)t.te_list.size());
+          t.tile_cptr.push_back((int)t.tc_rec.size() / 4);
+          cur = 0;
+        }
+        for (int e = cn_ptr[m]; e < cn_ptr[m + 1]; ++e) {
+          t.te_list.push_back(e);
+          t.te_chk.push_back(cur);
+          t.te_chk.push_back(cur + d);
+        }
+        t.tc_rec.insert(t.tc_rec.end(), {cur, d, cn_ptr[m], 0});
+        cur += d;
+      }
+      if (cur > 0) {
+        t.tile_eptr.push_back((int)t.te_list.size());
+        t.tile_cptr.push_back((int)t.tc_rec.size() / 4);
+      }
+      t.level_tptr.push_back((int)t.tile_eptr.size() - 1);
+    }
+  };
+  {
+    std::vector<int> all(M), one = {0, M};
+    for (int m = 0; m < M; ++m) all[m] = m;
+    build_tiling(ht[0], one, all);
+    build_tiling(ht[1], level_ptr, level_checks);
+  }
   // packed records and per-edge two-hop facts for the dynamic engine
   std::vector<int> ecv(2ull * E), vrec(2ull * N), vadj(4ull * E), erec(4ull * E), hop_n(E), hop_distinct(E);
   std::vector<uint8_t> hop_dup(E, 0);
@@ -533,6 +590,52 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     delete G;
     return LDPC_ERR_CUDA;
   }
+  // tilings: one more device block
+  {
+    size_t tot = 0;
+    for (auto& t : ht)
+      tot += t.level_tptr.size() + t.tile_eptr.size() + t.te_list.size() + t.te_chk.size() + t.tile_cptr.size() +
+             t.tc_rec.size() + 8;
+    int* tb = nullptr;
+    if (cudaMalloc(&tb, tot * sizeof(int)) != cudaSuccess) {
+      cudaFree(d);
+      delete G;
+      return LDPC_ERR_CUDA;
+    }
+    std::vector<int> hb;
+    hb.reserve(tot);
+    Tiling* dst[2] = {&G->flood, &G->layer};
+    for (int i = 0; i < 2; ++i) {
+      auto& t = ht[i];
+      while (hb.size() % 4) hb.push_back(0);  // int4 alignment of tc_rec
+      size_t o_rec = hb.size();
+      hb.insert(hb.end(), t.tc_rec.begin(), t.tc_rec.end());
+      size_t o_chk = hb.size();
+      hb.insert(hb.end(), t.te_chk.begin(), t.te_chk.end());
+      size_t o_lt = hb.size();
+      hb.insert(hb.end(), t.level_tptr.begin(), t.level_tptr.end());
+      size_t o_te = hb.size();
+      hb.insert(hb.end(), t.tile_eptr.begin(), t.tile_eptr.end());
+      size_t o_tl = hb.size();
+      hb.insert(hb.end(), t.te_list.begin(), t.te_list.end());
+      size_t o_cp = hb.size();
+      hb.insert(hb.end(), t.tile_cptr.begin(), t.tile_cptr.end());
+      dst[i]->tc_rec = (int4*)(tb + o_rec);
+      dst[i]->tile_cptr = tb + o_cp;
+      dst[i]->n_levels = (int)t.level_tptr.size() - 1;
+      dst[i]->te_chk = (int2*)(tb + o_chk);
+      dst[i]->level_tptr = tb + o_lt;
+      dst[i]->tile_eptr = tb + o_te;
+      dst[i]->te_list = tb + o_tl;
+    }
+    if (cudaMemcpy(tb, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(tb);
+      cudaFree(d);
+      delete G;
+      return LDPC_ERR_CUDA;
+    }
+    G->tile_block = tb;
+  }
   G->dev_block = d;
   G->max_dv = max_dv;
   G->max_dc = max_dc;
@@ -566,6 +669,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
 int ldpc_graph_destroy(ldpc_graph_t* G) {
   if (!G) return LDPC_ERR_INVALID;
   cudaFree(G->dev_block);
+  cudaFree(G->tile_block);
   delete G;
   return LDPC_OK;
 }
@@ -594,8 +698,8 @@ int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B,
       ws = pl.ws_bytes;
     } else {
       FixedPlan pl;
-      if (s->precision == LDPC_F64) fixed_plan<double>(G, s, B, pl);
-      else fixed_plan<float>(G, s, B, pl);
+      int rc = s->precision == LDPC_F64 ? fixed_plan<double>(G, s, B, pl) : fixed_plan<float>(G, s, B, pl);
+      if (rc) return rc;
       ws = pl.ws_bytes;
     }
   }

@@ -92,9 +92,14 @@ template <> struct Num<float> {
   static constexpr float kLlrMax = 30.0f;
   static constexpr float kAtanhClip = (float)(1.0 - 1e-12);  // rounds to 1.0f: fp32 saturates earlier
   static constexpr float kBig = 3.0e38f;
-  __device__ static float tanh_(float x) { return tanhf(x); }
-  __device__ static float atanh_(float x) { return atanhf(x); }
-  __device__ static float exp_(float x) { return expf(x); }
+  // fp32 fast mode (no bit-parity obligation; tested statistically): SFU forms
+  __device__ static float tanh_(float x) {
+    const float a = fabsf(x);
+    const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * a) + 1.0f);
+    return copysignf(a < 0.004f ? a : t, x);  // small |x|: tanh x = x to fp32 precision
+  }
+  __device__ static float atanh_(float x) { return 0.5f * __logf(__fdividef(1.0f + x, 1.0f - x)); }
+  __device__ static float exp_(float x) { return __expf(x); }
   __device__ static float abs_(float x) { return fabsf(x); }
   __device__ static Key key(float v) { return v >= 0.0f ? __float_as_uint(v) + 1u : 0u; }
 };
