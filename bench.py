@@ -41,6 +41,11 @@ WORKLOADS = {
                                    ("me_cirbp", 4), ("me_cirbp", 16)]),
     "C3": ("C3", 1.0, 10, 10_000, [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1),
                                    ("me_cirbp", 64)]),
+    # C4 = the C2 code at 0 dB, budget 20 E (batch/occupancy sweep: --batch)
+    "C4": ("C2", 0.0, 20, 16_384, [("me_cirbp", 1), ("me_cirbp", 4), ("me_cirbp", 16), ("me_cirbp", 64),
+                                   ("rbp", 1)]),
+    # BG1 fixed schedules only (the roofline case: HBM-bound frame-interleaved kernels)
+    "C3F": ("C3", 1.0, 10, 10_000, [("flooding", 1), ("layered", 1)]),
 }
 
 CI_KINDS = {"cirbp", "lmd_cirbp", "me_cirbp", "me_lmd_cirbp"}
@@ -157,12 +162,12 @@ def run_reference(args, wl):
         tot_t += t
     val = tot_u / tot_t
     line = {
-        "impl": "reference", "metric": "C2V edge updates/s (all C1 schedules); decoded frames/s",
+        "impl": "reference", "metric": f"C2V edge updates/s (all {args.workload} schedules); decoded frames/s",
         "value": val, "unit": "C2V edge updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "frames_per_s": tot_f / tot_t,
-        "config": {"workload": f"{key}: " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+        "config": {"workload": f"{args.workload} ({spec.label}): " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
                    "code": spec.label, "ebn0_db": ebn0, "i_max": i_max, "batch": sample},
         "cpu_baseline": {"value": val, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
                          "sample": f"first {sample} frames of the seeded batch, every schedule"},
@@ -173,30 +178,31 @@ def run_reference(args, wl):
 
 
 def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
-    """Oracle on a bounded sample, all host cores (rank 0, N=1 only)."""
+    """Oracle on a bounded sample of the same batch, all host cores (rank 0, N=1
+    only): first one frame per core through every schedule, then, if that took
+    less than the budget, a larger sample scaled to ~budget_s."""
     from oracle import pyoracle
     key, ebn0, i_max, batch, scheds = wl
     cores = os.cpu_count() or 1
-    # size the sample from a quick probe so the whole baseline takes ~budget_s
-    probe = llr_host[:cores * 4].astype(np.float64)
-    t0 = time.perf_counter()
-    for kind, n_p in scheds:
-        pyoracle.decode_batch(g, probe, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p, threads=cores)
-    dt = time.perf_counter() - t0
-    n = int(max(cores * 4, min(len(llr_host), len(probe) * budget_s / max(dt, 1e-3))))
-    sample = llr_host[:n].astype(np.float64)
-    per = {}
-    tot_u = 0
-    t0 = time.perf_counter()
-    for kind, n_p in scheds:
-        t1 = time.perf_counter()
-        r = pyoracle.decode_batch(g, sample, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
-                                  threads=cores)
-        u = int(r["prop"].sum())
-        per[f"{kind}" + (f"/M{n_p}" if n_p > 1 else "")] = u / (time.perf_counter() - t1)
-        tot_u += u
-    t = time.perf_counter() - t0
-    return {"value": tot_u / t, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
+
+    def run(sample):
+        per, tot_u = {}, 0
+        t0 = time.perf_counter()
+        for kind, n_p in scheds:
+            t1 = time.perf_counter()
+            r = pyoracle.decode_batch(g, sample, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
+                                      threads=cores)
+            u = int(r["prop"].sum())
+            per[f"{kind}" + (f"/M{n_p}" if n_p > 1 else "")] = u / (time.perf_counter() - t1)
+            tot_u += u
+        return tot_u, time.perf_counter() - t0, per
+
+    n = min(len(llr_host), cores)
+    u, t, per = run(llr_host[:n].astype(np.float64))
+    if t < budget_s / 2 and n < len(llr_host):
+        n = int(min(len(llr_host), max(n, n * budget_s / max(t, 1e-3)) // cores * cores))
+        u, t, per = run(llr_host[:n].astype(np.float64))
+    return {"value": u / t, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
             "sample": f"first {n} frames of the batch through every schedule ({t:.1f} s)",
             "frames_per_s": n * len(scheds) / t, "per_schedule_updates_per_s": per}
 
@@ -204,6 +210,7 @@ def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
 def run_ours(args, wl):
     import torch
     from paper_2102_11089_b200 import configs
+    from paper_2102_11089_b200 import dist as D
     from paper_2102_11089_b200.codes import build_tanner
     from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch, device_graph
 
@@ -221,7 +228,8 @@ def run_ours(args, wl):
     E, N = g.n_edges, g.n_vars
     elem = 8 if args.precision == "f64" else 4
     dev = torch.device("cuda", torch.cuda.current_device())
-    llr_host = make_inputs(spec, ebn0, rank * batch, batch)
+    start, _ = D.shard(batch, rank)  # weak scaling: disjoint frame-index ranges per rank
+    llr_host = make_inputs(spec, ebn0, start, batch)
     llr_pinned = torch.from_numpy(llr_host).pin_memory()
     llr_dev = llr_pinned.to(dev)
     cfgs = [ScheduleConfig(kind=k, i_max=i_max, n_p=n_p, precision=args.precision) for k, n_p in scheds]
@@ -287,15 +295,9 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end)
 
-    step_updates = sum(w["updates"] for w in work)
-    t_max = total_ms
-    e_max = e2e_ms
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([total_ms, e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max, e_max = tt.tolist()
-    job_updates = step_updates * args.steps * world
+    step_updates = int(D.all_sum([sum(w["updates"] for w in work)])[0])  # all ranks
+    t_max, e_max = (float(x) for x in D.all_max([total_ms, e2e_ms]))
+    job_updates = step_updates * args.steps
     value = job_updates / (t_max / 1e3)
     e2e_value = job_updates / (e_max / 1e3)
 
@@ -322,12 +324,12 @@ def run_ours(args, wl):
                    "updates_per_frame": wk["updates"] / batch, "state_bytes_per_update": round(wk["bpu"], 1),
                    "state_GBps": wk["updates"] * wk["bpu"] / (sched_ms[i] / 1e3) / 1e9}
     line = {
-        "metric": "C2V edge updates/s (all C1 schedules); decoded frames/s",
+        "metric": f"C2V edge updates/s (all {args.workload} schedules); decoded frames/s",
         "value": value, "unit": "C2V edge updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "frames_per_s": batch * len(cfgs) * args.steps * world / (t_max / 1e3),
-        "config": {"workload": f"{key}: " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+        "config": {"workload": f"{args.workload} ({spec.label}): " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
                    "code": spec.label, "N": N, "E": E, "ebn0_db": ebn0, "i_max": i_max,
                    "batch_per_gpu": batch, "l2": "inputs > L2 (batch LLRs %.0f MB)" % (llr_pinned.numel() * 4 / 1e6),
                    "parallelism": f"frames sharded over {world} GPU(s)"},

@@ -36,7 +36,11 @@
 
 namespace ldpc {
 
-constexpr int kFlatCiMax = 1024;  // CIRBP: flat CI argmax when N <= this
+#ifndef LDPC_DYN_MIN_BLOCKS
+#define LDPC_DYN_MIN_BLOCKS 4
+#endif
+
+constexpr int kFlatCiMax = 128;  // CIRBP: flat CI argmax when N <= this (else incremental tree)
 
 struct DynParams {
   DevGraph g;
@@ -81,7 +85,8 @@ struct Ctx {
   int *ridx, *cidx;    // level-1 argmax leaf of each 32-leaf group
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
   int *members, *sel, *chosen;
-  int4* items;    // two-hop edges of the last update (g, a, d, stage base), ascending g
+  const int4* items;  // two-hop edges of the last update (g, a, d, stage base), ascending g
+  int4* items_buf;    // per-warp scratch for items built on the fly
   T* stage;       // staged check inputs of the last update
   Key* nk;        // new residual key of each item
   int *dl0, *dl1; // dirty-node lists for tree maintenance
@@ -318,7 +323,7 @@ __device__ __forceinline__ int build_items_from(Ctx<T>& c, int4 adj, bool act, i
   if (act) {
     int t = t0;
     for (int e = adj.z; e < adj.w; ++e)
-      if (e != adj.x) c.items[t++] = make_int4(e, adj.z, d, sbase);
+      if (e != adj.x) c.items_buf[t++] = make_int4(e, adj.z, d, sbase);
   }
   *sbase_out = sbase;
   return total;
@@ -326,6 +331,11 @@ __device__ __forceinline__ int build_items_from(Ctx<T>& c, int4 adj, bool act, i
 
 template <typename T>
 __device__ int build_items(const DevGraph& g, Ctx<T>& c, int e_star) {
+  if (g.hop_items) {  // precomputed table
+    c.items = g.hop_items + g.hop_ptr[e_star];
+    return g.hop_n[e_star];
+  }
+  c.items = c.items_buf;
   int2 mn = g.ecv[e_star];
   int2 vr = g.vrec[mn.y];
   int4 adj = make_int4(-1, -1, 0, 0);
@@ -382,8 +392,15 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
       c.ci[n_star] = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
     }
   }
-  int sbase;
-  const int n_items = build_items_from<T>(c, adj, act, &sbase);
+  int sbase, n_items;
+  if (g.hop_items) {  // precomputed two-hop records and stage bases
+    c.items = g.hop_items + g.hop_ptr[e_star];
+    n_items = g.hop_n[e_star];
+    sbase = lane < vr.y ? g.hop_sb[g.hop_sbptr[e_star] + lane] : 0;
+  } else {
+    c.items = c.items_buf;
+    n_items = build_items_from<T>(c, adj, act, &sbase);
+  }
   if (act) {  // V2C to the other checks of n* (E:153-160), also staged
     T v = clampv(tot - cf);
     T th = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
@@ -1067,7 +1084,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
 // MODE 0: E, N and T parts in shared memory; 1: E in HBM, N and T in shared;
 // 2: E and N in HBM, T in shared; 3: everything in HBM.
 template <typename T, int KERNEL, int MODE, int KF>
-__global__ void __launch_bounds__(256) dyn_decode_kernel(const __grid_constant__ DynParams p) {
+__global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const long long gw = (long long)blockIdx.x * wpb + warp;
@@ -1101,7 +1118,8 @@ __global__ void __launch_bounds__(256) dyn_decode_kernel(const __grid_constant__
   c.ridx = (int*)(bT + p.o_ridx);
   c.ctree = (Key*)(bT + p.o_ctree);
   c.cidx = (int*)(bT + p.o_cidx);
-  c.items = (int4*)(scr + p.so_items);
+  c.items_buf = (int4*)(scr + p.so_items);
+  c.items = c.items_buf;
   c.stage = (T*)(scr + p.so_stage);
   c.nk = (Key*)(scr + p.so_nk);
   c.dl0 = (int*)(scr + p.so_dl0);

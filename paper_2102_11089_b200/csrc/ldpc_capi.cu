@@ -31,6 +31,7 @@ struct ldpc_graph {
   int max_dv, max_dc, max_items;
   Tiling flood, layer;
   int* tile_block;
+  unsigned char* hop_block;  // precomputed two-hop tables (may be null)
 };
 
 namespace {
@@ -555,6 +556,34 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       hop_dup[e] = distinct < cnt ? 1 : 0;
     }
   }
+  // precomputed two-hop tables (item records + per-slot stage bases), if <= 256 MB
+  std::vector<long long> hop_ptr(E + 1, 0);
+  std::vector<int> hop_sbptr(E + 1, 0);
+  for (int e = 0; e < E; ++e) {
+    hop_ptr[e + 1] = hop_ptr[e] + hop_n[e];
+    hop_sbptr[e + 1] = hop_sbptr[e] + (vn_ptr[edge_vn[e] + 1] - vn_ptr[edge_vn[e]]);
+  }
+  const bool want_tab = hop_ptr[E] * 16 + (long long)hop_sbptr[E] * 4 <= (256ll << 20);
+  std::vector<int> hop_items, hop_sb;
+  if (want_tab) {
+    hop_items.reserve(4 * hop_ptr[E]);
+    hop_sb.reserve(hop_sbptr[E]);
+    for (int e = 0; e < E; ++e) {
+      const int m_star = edge_cn[e], n_star = edge_vn[e];
+      int sb = 0;
+      for (int k = vn_ptr[n_star]; k < vn_ptr[n_star + 1]; ++k) {
+        const int f = vn_edges[k], i = edge_cn[f], a = cn_ptr[i], b = cn_ptr[i + 1];
+        if (i == m_star) {
+          hop_sb.push_back(-1);
+          continue;
+        }
+        hop_sb.push_back(sb);
+        for (int g2 = a; g2 < b; ++g2)
+          if (g2 != f) hop_items.insert(hop_items.end(), {g2, a, b - a, sb});
+        sb += b - a;
+      }
+    }
+  }
   // one device block (int units): edge_cn, edge_vn, vn_edges [E]; cn_ptr [M+1];
   // vn_ptr [N+1]; level_ptr [L+1]; level_checks [M]; ecv [2E]; vrec [2N];
   // vadj [4E] (16-byte aligned); hop_n [E]; hop_distinct [E]; hop_dup [E bytes]
@@ -636,6 +665,34 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     }
     G->tile_block = tb;
   }
+  if (want_tab) {  // two-hop tables: their own allocation
+    const size_t bytes = hop_items.size() * 4 + (size_t)E * 8 + (size_t)E * 4 + hop_sb.size() * 4 + 64;
+    unsigned char* hb = nullptr;
+    if (cudaMalloc(&hb, bytes) != cudaSuccess) {
+      cudaFree(G->tile_block);
+      cudaFree(d);
+      delete G;
+      return LDPC_ERR_CUDA;
+    }
+    size_t o_items = 0, o_ptr = align16(hop_items.size() * 4), o_sbp = o_ptr + (size_t)E * 8,
+           o_sb = o_sbp + (size_t)E * 4;
+    bool ok = cudaMemcpy(hb + o_items, hop_items.data(), hop_items.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(hb + o_ptr, hop_ptr.data(), (size_t)E * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(hb + o_sbp, hop_sbptr.data(), (size_t)E * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(hb + o_sb, hop_sb.data(), hop_sb.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+      cudaFree(hb);
+      cudaFree(G->tile_block);
+      cudaFree(d);
+      delete G;
+      return LDPC_ERR_CUDA;
+    }
+    G->hop_block = hb;
+    G->d.hop_items = (const int4*)(hb + o_items);
+    G->d.hop_ptr = (const long long*)(hb + o_ptr);
+    G->d.hop_sbptr = (const int*)(hb + o_sbp);
+    G->d.hop_sb = (const int*)(hb + o_sb);
+  }
   G->dev_block = d;
   G->max_dv = max_dv;
   G->max_dc = max_dc;
@@ -670,6 +727,7 @@ int ldpc_graph_destroy(ldpc_graph_t* G) {
   if (!G) return LDPC_ERR_INVALID;
   cudaFree(G->dev_block);
   cudaFree(G->tile_block);
+  if (G->hop_block) cudaFree(G->hop_block);
   delete G;
   return LDPC_OK;
 }

@@ -43,6 +43,11 @@ struct DevGraph {
   const int* hop_n;         // [E]  two-hop set size of e (pre-C2V refreshes when e propagates)
   const int* hop_distinct;  // [E]  distinct VNs in that set (E:536-549 candidate count)
   const uint8_t* hop_dup;   // [E]  1 if a VN repeats in that set (4-cycle through n*)
+  // optional precomputed two-hop tables (null when they would be too large):
+  const long long* hop_ptr; // [E]  offset of e's item records in hop_items
+  const int4* hop_items;    // item records (g, check start, check degree, stage base)
+  const int* hop_sbptr;     // [E]  offset of e's per-VN-slot stage bases in hop_sb
+  const int* hop_sb;        // stage base of each vn_edges slot of vn(e) (-1 for cn(e))
 };
 
 // 32-ary max-tree geometry over `n` leaves (levels 1..L; level L has <= 64 nodes,
