@@ -121,6 +121,15 @@ int ldpc_set_step_log(int64_t* dev_log, int32_t cap);
  * step < 0 disables. */
 int ldpc_set_state_dump(int64_t step, double* dev_buf);
 
+/* On-GPU BPSK/AWGN frames (channel.py:35-86 conventions): out[B][N] (float32,
+ * or float64 if out_f64) = clip(2y/sigma^2, +-30) with y = 1 + sigma*z for
+ * the transmitted positions n >= n_punct_prefix and 0 for the punctured
+ * prefix; frame f uses the counter-based stream keyed by (seed, start + f)
+ * (Philox4x32-10 + Box-Muller; statistically equivalent to the host
+ * generator, not bit-identical). */
+int ldpc_generate_awgn(int32_t N, int32_t n_punct_prefix, int64_t B, double sigma, uint64_t seed,
+                       int64_t start, void* out, int32_t out_f64, void* cuda_stream);
+
 /* Number of kernel launches the last ldpc_decode on this thread issued. */
 int ldpc_last_launch_count(void);
 

@@ -28,6 +28,7 @@ class LdpcSched(C.Structure):
 # every exported symbol of include/ldpc_b200.h
 EXPORTS = ("ldpc_graph_create", "ldpc_graph_destroy", "ldpc_graph_info", "ldpc_workspace_size",
            "ldpc_decode", "ldpc_select_vns", "ldpc_set_step_log", "ldpc_set_state_dump",
+           "ldpc_generate_awgn",
            "ldpc_last_launch_count",
            "ldpc_strerror", "ldpc_version")
 
@@ -55,6 +56,7 @@ def lib():
     L.ldpc_decode.argtypes = [P, P, I64, C.POINTER(LdpcSched)] + [P] * 8 + [P, SZ, P]
     L.ldpc_select_vns.argtypes = [P, P, I32, I32, I32, I64, P, P, P]
     L.ldpc_set_step_log.argtypes = [P, I32]
+    L.ldpc_generate_awgn.argtypes = [I32, I32, I64, C.c_double, C.c_uint64, I64, P, I32, P]
     L.ldpc_set_state_dump.argtypes = [I64, P]
     L.ldpc_last_launch_count.argtypes = []
     L.ldpc_strerror.argtypes = [C.c_int]

@@ -103,3 +103,32 @@ def llr_batch(code, ebn0_db, seed, start, count, dtype=np.float32):
         y = 1.0 + rng.normal(0.0, cfg.sigma, size=n_tx)
         out[b, tx] = np.clip(2.0 * y / s2, -LLR_MAX, LLR_MAX)
     return out
+
+
+def llr_batch_device(code, ebn0_db, seed, start, count, dtype=None, device=None, stream=None):
+    """[count, N] channel LLRs generated on the GPU (csrc/channel_gen.cu).
+
+    Same channel model, LLR clip and puncturing as llr_batch and frames keyed
+    by (seed, frame index), but a counter-based Philox4x32 + Box-Muller stream:
+    statistically equivalent to the host generator, not bit-identical.  Needs
+    prefix puncturing (apply_puncture).
+    """
+    import ctypes as C
+
+    import torch
+
+    from . import _native
+    p = len(code.punctured)
+    if tuple(code.punctured) != tuple(range(p)):
+        raise ValueError("on-GPU generation supports prefix puncturing only")
+    dtype = dtype or torch.float32
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((count, code.h.n_cols), dtype=dtype, device=device)
+    st = stream if stream is not None else torch.cuda.current_stream(device)
+    sigma = ebn0_to_sigma(ebn0_db, code)
+    _native.check(_native.lib().ldpc_generate_awgn(code.h.n_cols, p, count, sigma, int(seed) & (2**64 - 1),
+                                                   start, C.c_void_p(out.data_ptr()),
+                                                   1 if dtype == torch.float64 else 0,
+                                                   C.c_void_p(st.cuda_stream)),
+                  "ldpc_generate_awgn")
+    return out

@@ -77,9 +77,10 @@ struct DynParams {
   int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes;
 };
 
-template <typename T>
+template <typename T, int G>
 struct Ctx {
   using Key = typename Num<T>::Key;
+  Grp<G> w;            // this frame's lane group
   T *c2v, *pre, *in, *res, *total, *pretot, *ci, *p0t, *tmp;  // p0t = p0(total), CI kinds
   Key *rtree, *ctree;  // tree node keys, all levels
   int *ridx, *cidx;    // level-1 argmax leaf of each 32-leaf group
@@ -97,13 +98,13 @@ struct Ctx {
   int nsel;          // Alg.-4 selections made (debug log index)
   long long next_b;  // next single-edge iteration boundary (k * E)
   int it;            // completed iterations
-  int lane;
+  int lane;          // lane within the group (= w.lane)
   long long rng;
 };
 
 // residual leaf key: |pre - c2v| (or the stored residual for ME-RBP's exclusion)
-template <typename T, bool STORED>
-__device__ __forceinline__ typename Num<T>::Key res_key(const Ctx<T>& c, int e) {
+template <typename T, bool STORED, int G>
+__device__ __forceinline__ typename Num<T>::Key res_key(const Ctx<T, G>& c, int e) {
   if (STORED) return Num<T>::key(c.res[e]);
   return Num<T>::key(Num<T>::abs_(c.pre[e] - c.c2v[e]));
 }
@@ -121,17 +122,25 @@ __device__ __forceinline__ Key child_key(const Key* tree, const TreeGeom& geo, i
   return tree[geo.off[level] + child];
 }
 
-__device__ __forceinline__ unsigned long long warp_max_only(unsigned long long k) {
-  unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
-  unsigned mh = __reduce_max_sync(kFull, hi);
-  unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
-  return ((unsigned long long)mh << 32) | ml;
+// lane-local scan of node q's 32 children (level l-1), strided by the group
+// width; returns the lane's (max key, lowest child index among ties)
+template <int G, typename Key, typename LeafFn>
+__device__ __forceinline__ Key child_scan(const Key* tree, const TreeGeom& geo, int l, int q, int lane,
+                                          LeafFn leaf, int* bi) {
+  Key m = 0;
+  int b = 0x7fffffff;
+#pragma unroll
+  for (int c = lane; c < 32; c += G) {
+    const Key k = child_key(tree, geo, l - 1, q * 32 + c, leaf);
+    if (k > m || b == 0x7fffffff) { m = k; b = q * 32 + c; }
+  }
+  *bi = b;
+  return m;
 }
-__device__ __forceinline__ unsigned warp_max_only(unsigned k) { return __reduce_max_sync(kFull, k); }
 
-template <typename Key, typename LeafFn>
-__device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, int lane, LeafFn leaf) {
-  for (int q = lane; q < geo.size[1]; q += 32) {
+template <int G, typename Key, typename LeafFn>
+__device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, const Grp<G>& w, LeafFn leaf) {
+  for (int q = w.lane; q < geo.size[1]; q += G) {
     Key m = 0;
     int bi = q * 32;
     for (int c = 0; c < 32; ++c) {
@@ -141,9 +150,9 @@ __device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, int lane, 
     tree[geo.off[1] + q] = m;
     idx1[q] = bi;
   }
-  __syncwarp();
+  w.sync();
   for (int l = 2; l <= geo.levels; ++l) {
-    for (int q = lane; q < geo.size[l]; q += 32) {
+    for (int q = w.lane; q < geo.size[l]; q += G) {
       Key m = 0;
       for (int c = 0; c < 32; ++c) {
         Key k = child_key(tree, geo, l - 1, q * 32 + c, leaf);
@@ -151,60 +160,61 @@ __device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, int lane, 
       }
       tree[geo.off[l] + q] = m;
     }
-    __syncwarp();
+    w.sync();
   }
 }
 
-// Full recompute of level-1 group q from its leaves (warp-cooperative).
-template <typename Key, typename LeafFn>
-__device__ __forceinline__ void group_recompute(Key* tree, int* idx1, const TreeGeom& geo, int q, int lane,
-                                                LeafFn leaf) {
-  int e = q * 32 + lane;
-  Key k = child_key(tree, geo, 0, e, leaf);
+// Full recompute of level-1 group q from its leaves (group-cooperative).
+template <int G, typename Key, typename LeafFn>
+__device__ __forceinline__ void group_recompute(Key* tree, int* idx1, const TreeGeom& geo, int q,
+                                                const Grp<G>& w, LeafFn leaf) {
+  int bi;
+  const Key k = child_scan<G>(tree, geo, 1, q, w.lane, leaf, &bi);
   int best;
-  Key m = warp_max_key_minidx(k, e, &best);
-  if (lane == 0) {
+  const Key m = w.max_key_minidx(k, bi, &best);
+  if (w.lane == 0) {
     tree[geo.off[1] + q] = m;
     idx1[q] = best;
   }
 }
 
 // Recompute the ancestors (levels >= 2) of the level-1 groups dl[0..n).
-template <typename Key, typename LeafFn>
-__device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int* dl2, int n, int lane,
+template <int G, typename Key, typename LeafFn>
+__device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int* dl2, int n, const Grp<G>& w,
                                    LeafFn leaf) {
   for (int l = 2; l <= geo.levels; ++l) {
     int cnt = 0;
-    for (int base = 0; base < n; base += 32) {
-      int idx = base + lane;
+    for (int base = 0; base < n; base += G) {
+      int idx = base + w.lane;
       int v = idx < n ? (dl[idx] >> 5) : -1;
       int pv = (idx > 0 && idx < n) ? (dl[idx - 1] >> 5) : -2;
       bool keep = idx < n && v != pv;
-      unsigned bal = __ballot_sync(kFull, keep);
-      if (keep) dl2[cnt + __popc(bal & lanemask_lt())] = v;
+      unsigned bal = w.ballot(keep);
+      if (keep) dl2[cnt + __popc(bal & w.lt)] = v;
       cnt += __popc(bal);
     }
-    __syncwarp();
+    w.sync();
     int* t = dl;
     dl = dl2;
     dl2 = t;
     n = cnt;
     for (int i = 0; i < n; ++i) {
-      int q = dl[i];
-      Key m = warp_max_only(child_key(tree, geo, l - 1, q * 32 + lane, leaf));
-      if (lane == 0) tree[geo.off[l] + q] = m;
+      const int q = dl[i];
+      int bi;
+      const Key m = w.max_key_only(child_scan<G>(tree, geo, l, q, w.lane, leaf, &bi));
+      if (w.lane == 0) tree[geo.off[l] + q] = m;
     }
-    __syncwarp();
+    w.sync();
   }
 }
 
 // Full recompute of the level-1 groups dl[0..n) and their ancestors.
-template <typename Key, typename LeafFn>
+template <int G, typename Key, typename LeafFn>
 __device__ void tree_update_list(Key* tree, int* idx1, const TreeGeom& geo, int* dl, int* dl2, int n,
-                                 int lane, LeafFn leaf) {
-  for (int i = 0; i < n; ++i) group_recompute(tree, idx1, geo, dl[i], lane, leaf);
-  __syncwarp();
-  tree_fix_ancestors(tree, geo, dl, dl2, n, lane, leaf);
+                                 const Grp<G>& w, LeafFn leaf) {
+  for (int i = 0; i < n; ++i) group_recompute(tree, idx1, geo, dl[i], w, leaf);
+  w.sync();
+  tree_fix_ancestors(tree, geo, dl, dl2, n, w, leaf);
 }
 
 // Incremental rule for one leaf e of group q getting key kk, applied to the
@@ -226,15 +236,15 @@ __device__ __forceinline__ bool leaf_rule(Key& Q, int& I, int e, Key kk) {
 // Incremental update of level-1 groups for per-lane leaf changes (leaf e or
 // -1, new key kk), lanes of the same group serialised by a match_any leader.
 // Appends groups to recompute to rec[] and changed groups to dirty[].
-template <typename Key>
-__device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Key kk, int lane, int* se,
+template <int G, typename Key>
+__device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Key kk, const Grp<G>& w, int* se,
                                                    Key* sk, int* rec, int& nrec, int* dirty, int& ndirty) {
   const int q = e >= 0 ? (e >> 5) : -1;
-  se[lane] = e;
-  sk[lane] = kk;
-  __syncwarp();
-  const unsigned peers = __match_any_sync(kFull, q);
-  const bool leader = e >= 0 && (__ffs(peers) - 1) == lane;
+  se[w.lane] = e;
+  sk[w.lane] = kk;
+  w.sync();
+  const unsigned peers = w.match_any(q);
+  const bool leader = e >= 0 && (__ffs(peers) - 1) == w.lane;
   bool r = false, changed = false;
   if (leader) {
     Key Q = L1[q];
@@ -253,27 +263,33 @@ __device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Ke
     }
     changed = r || Q != Q0;
   }
-  const unsigned rb = __ballot_sync(kFull, r), cb = __ballot_sync(kFull, changed);
-  if (r) rec[nrec + __popc(rb & lanemask_lt())] = q;
-  if (changed) dirty[ndirty + __popc(cb & lanemask_lt())] = q;
+  const unsigned rb = w.ballot(r), cb = w.ballot(changed);
+  if (r) rec[nrec + __popc(rb & w.lt)] = q;
+  if (changed) dirty[ndirty + __popc(cb & w.lt)] = q;
   nrec += __popc(rb);
   ndirty += __popc(cb);
-  __syncwarp();
+  w.sync();
 }
 
-template <typename Key, typename LeafFn>
-__device__ int tree_argmax(const Key* tree, const int* idx1, const TreeGeom& geo, int lane, LeafFn leaf) {
+template <int G, typename Key, typename LeafFn>
+__device__ int tree_argmax(const Key* tree, const int* idx1, const TreeGeom& geo, const Grp<G>& w,
+                           LeafFn leaf) {
   const int L = geo.levels, s = geo.size[L];
   const Key* top = tree + geo.off[L];
-  Key k0 = lane < s ? top[lane] : Key(0);
-  Key k1 = lane + 32 < s ? top[lane + 32] : Key(0);
+  Key bk = 0;
+  int bq = 0x7fffffff;
+  for (int i = w.lane; i < s; i += G) {  // top level (<= 64 nodes)
+    const Key k = top[i];
+    if (k > bk || bq == 0x7fffffff) { bk = k; bq = i; }
+  }
   int q;
-  warp_max_key_minidx(k1 > k0 ? k1 : k0, k1 > k0 ? lane + 32 : lane, &q);
+  w.max_key_minidx(bk, bq, &q);
   for (int l = L - 1; l >= 1; --l) {
-    Key k = child_key(tree, geo, l, q * 32 + lane, leaf);
-    int ln;
-    warp_max_key(k, &ln);
-    q = q * 32 + ln;
+    int bi;
+    const Key k = child_scan<G>(tree, geo, l + 1, q, w.lane, leaf, &bi);
+    int best;
+    w.max_key_minidx(k, bi, &best);
+    q = best;
   }
   return idx1[q];
 }
@@ -281,28 +297,33 @@ __device__ int tree_argmax(const Key* tree, const int* idx1, const TreeGeom& geo
 // ------------------------------------------------------------ argmax scans
 
 // E:260-266 -- first maximum of key(i) over i in [0, n)
-template <typename Key, typename KeyFn>
-__device__ int argmax_scan(int n, int lane, KeyFn keyf) {
+template <typename Key, int G, typename KeyFn>
+__device__ int argmax_scan(int n, const Grp<G>& w, KeyFn keyf) {
   Key best = 0;
   int bi = 0x7fffffff;
-  for (int i = lane; i < n; i += 32) {
+  for (int i = w.lane; i < n; i += G) {
     Key k = keyf(i);
     if (k > best) { best = k; bi = i; }
   }
   int idx;
-  warp_max_key_minidx(best, bi, &idx);
+  w.max_key_minidx(best, bi, &idx);
   return idx;
 }
 
 // E:269-276 -- first maximum residual over M(n) in vn_edges order (= edge order)
-template <typename T>
-__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T>& c, int n, int lane) {
+template <typename T, int G>
+__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T, G>& c, int n) {
   using Key = typename Num<T>::Key;
-  int2 vr = g.vrec[n];
-  int e = lane < vr.y ? g.vn_edges[vr.x + lane] : 0x7fffffff;
-  Key k = lane < vr.y ? res_key<T, false>(c, e) : Key(0);
+  const int2 vr = g.vrec[n];
+  Key bk = 0;
+  int be = 0x7fffffff;
+  for (int k = c.lane; k < vr.y; k += G) {  // vn_edges ascend: first max = lowest edge
+    const int e = g.vn_edges[vr.x + k];
+    const Key kk = res_key<T, false, G>(c, e);
+    if (kk > bk || be == 0x7fffffff) { bk = kk; be = e; }
+  }
   int idx;
-  warp_max_key_minidx(k, e, &idx);
+  c.w.max_key_minidx(bk, be, &idx);
   return idx;
 }
 
@@ -313,36 +334,43 @@ __device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T>& 
 // record (lane < d_v), `act` = its check is not m*.  Also lays out the stage
 // area: check k's inputs at stage[sbase_k + (e - a_k)].  Returns the count;
 // the caller must __syncwarp() before reading the table.
-template <typename T>
-__device__ __forceinline__ int build_items_from(Ctx<T>& c, int4 adj, bool act, int* sbase_out) {
+template <typename T, int G>
+__device__ __forceinline__ int build_items_from(Ctx<T, G>& c, int4 adj, bool act, int* sbase_out,
+                                                int& carry_items, int& carry_stage) {
   const int d = act ? adj.w - adj.z : 0;
   const int packed = act ? ((d - 1) | (d << 16)) : 0;
-  const int incl = warp_incl_scan(packed);
-  const int total = __shfl_sync(kFull, incl, 31) & 0xffff;
-  const int t0 = (incl - packed) & 0xffff, sbase = (incl - packed) >> 16;
+  const int incl = c.w.incl_scan(packed);
+  const int total = c.w.shfl(incl, G - 1);
+  const int t0 = carry_items + ((incl - packed) & 0xffff), sbase = carry_stage + ((incl - packed) >> 16);
   if (act) {
     int t = t0;
     for (int e = adj.z; e < adj.w; ++e)
       if (e != adj.x) c.items_buf[t++] = make_int4(e, adj.z, d, sbase);
   }
   *sbase_out = sbase;
-  return total;
+  carry_items += total & 0xffff;
+  carry_stage += total >> 16;
+  return carry_items;
 }
 
-template <typename T>
-__device__ int build_items(const DevGraph& g, Ctx<T>& c, int e_star) {
-  if (g.hop_items) {  // precomputed table
+// item table of e (precomputed, or built into the group's scratch)
+template <typename T, int G>
+__device__ int build_items(const DevGraph& g, Ctx<T, G>& c, int e_star) {
+  if (g.hop_items) {
     c.items = g.hop_items + g.hop_ptr[e_star];
     return g.hop_n[e_star];
   }
   c.items = c.items_buf;
-  int2 mn = g.ecv[e_star];
-  int2 vr = g.vrec[mn.y];
-  int4 adj = make_int4(-1, -1, 0, 0);
-  if (c.lane < vr.y) adj = g.vadj[vr.x + c.lane];
-  int sb;
-  int n = build_items_from<T>(c, adj, c.lane < vr.y && adj.y != mn.x, &sb);
-  __syncwarp();
+  const int2 mn = g.ecv[e_star];
+  const int2 vr = g.vrec[mn.y];
+  int ci = 0, cs = 0, n = 0, sb;
+  for (int k0 = 0; k0 < vr.y; k0 += G) {
+    const int k = k0 + c.lane;
+    int4 adj = make_int4(-1, -1, 0, 0);
+    if (k < vr.y) adj = g.vadj[vr.x + k];
+    n = build_items_from<T, G>(c, adj, k < vr.y && adj.y != mn.x, &sb, ci, cs);
+  }
+  c.w.sync();
   return n;
 }
 
@@ -351,10 +379,11 @@ __device__ int build_items(const DevGraph& g, Ctx<T>& c, int e_star) {
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
 // pre-C2V (and, for CI schedules, pre_total / CI) state.  Leaves the item
 // table of e* for the LMD searches.
-template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED>
-__device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
+template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G>
+__device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
+  const Grp<G>& w = c.w;
   const int lane = c.lane;
   const int4 er = g.erec[e_star];  // (m*, n*, vn_ptr[n*], d_v(n*))
   const int m_star = er.x, n_star = er.y;
@@ -368,16 +397,16 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
   const T cf = act ? c.c2v[adj.x] : T(0);
   if (p.dump_buf && c.cur_f == 0 && c.prop == p.dump_step) {
     if (CI)
-      for (int n = lane; n < g.N; n += 32) {
+      for (int n = lane; n < g.N; n += G) {
         p.dump_buf[n] = (double)c.ci[n];
         p.dump_buf[g.N + n] = (double)c.pretot[n];
       }
-    for (int e = lane; e < g.E; e += 32) {
+    for (int e = lane; e < g.E; e += G) {
       p.dump_buf[2 * g.N + 8192 + e] = (double)c.pre[e];
       p.dump_buf[2 * g.N + 8192 + g.E + e] = (double)c.c2v[e];
     }
   }
-  __syncwarp();
+  w.sync();
   if (lane == 0) {
     if (p.step_log && c.prop < p.log_cap) {  // (edge, committed value bits) pairs
       p.step_log[2 * (c.cur_f * p.log_cap + c.prop)] = e_star;
@@ -392,30 +421,47 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
       c.ci[n_star] = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
     }
   }
-  int sbase, n_items;
-  if (g.hop_items) {  // precomputed two-hop records and stage bases
+  // V2C to the other checks of n* (E:153-160), also staged; slots in chunks of G
+  int n_items = 0, ci_ = 0, cs_ = 0;
+  if (g.hop_items) {
     c.items = g.hop_items + g.hop_ptr[e_star];
     n_items = g.hop_n[e_star];
-    sbase = lane < vr.y ? g.hop_sb[g.hop_sbptr[e_star] + lane] : 0;
   } else {
     c.items = c.items_buf;
-    n_items = build_items_from<T>(c, adj, act, &sbase);
   }
-  if (act) {  // V2C to the other checks of n* (E:153-160), also staged
-    T v = clampv(tot - cf);
-    T th = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
-    c.in[adj.x] = th;
-    c.stage[sbase + (adj.x - adj.z)] = th;
+  for (int k0 = 0; k0 < vr.y; k0 += G) {
+    int4 a2 = adj;
+    bool act2 = act;
+    T cf2 = cf;
+    if (k0 > 0) {
+      const int k = k0 + lane;
+      a2 = make_int4(-1, -1, 0, 0);
+      if (k < vr.y) a2 = g.vadj[vr.x + k];
+      act2 = k < vr.y && a2.y != m_star;
+      cf2 = act2 ? c.c2v[a2.x] : T(0);
+    }
+    int sbase = 0;
+    if (g.hop_items) {
+      if (k0 + lane < vr.y) sbase = g.hop_sb[g.hop_sbptr[e_star] + k0 + lane];
+    } else {
+      n_items = build_items_from<T, G>(c, a2, act2, &sbase, ci_, cs_);
+    }
+    if (act2) {
+      const T v = clampv(tot - cf2);
+      const T th = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+      c.in[a2.x] = th;
+      c.stage[sbase + (a2.x - a2.z)] = th;
+    }
   }
-  __syncwarp();
-  for (int t = lane; t < n_items; t += 32) {  // stage the rest of each check
+  w.sync();
+  for (int t = lane; t < n_items; t += G) {  // stage the rest of each check
     int4 r = c.items[t];
     c.stage[r.w + (r.x - r.y)] = c.in[r.x];
   }
-  __syncwarp();
+  w.sync();
   const bool dup = CI && g.hop_dup[e_star] != 0;
-  // two-hop refresh (E:161-176), 32 edges per pass in reference order
-  for (int base = 0; base < n_items; base += 32) {
+  // two-hop refresh (E:161-176), G edges per pass in reference order
+  for (int base = 0; base < n_items; base += G) {
     const int t = base + lane;
     const bool valid = t < n_items;
     int j = -1;
@@ -462,23 +508,23 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
         }
       } else {
         // the same VN reached through two checks (4-cycle): keep the reference's order
-        unsigned peers = __match_any_sync(kFull, j);
-        int rank = __popc(peers & lanemask_lt());
-        int maxrank = __reduce_max_sync(kFull, valid ? (unsigned)rank : 0u);
+        const unsigned peers = w.match_any(j);
+        const int rank = __popc(peers & w.lt);
+        const int maxrank = (int)w.rmax(valid ? (unsigned)rank : 0u);
         for (int r = 0; r <= maxrank; ++r) {
           if (valid && rank == r) c.pretot[j] += delta;
-          __syncwarp();
+          w.sync();
         }
-        bool last = valid && ((peers >> lane) >> 1) == 0;
+        const bool last = valid && ((peers >> lane) >> 1) == 0;
         if (last) c.ci[j] = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
       }
     }
   }
-  __syncwarp();
+  w.sync();
   if (RT) {
     // incremental residual-tree update: e* first (residual -> 0), then one
-    // leader lane per 32-leaf group of the (ascending) items applies the leaf
-    // rule; groups whose argmax leaf decreased are recomputed from leaves.
+    // segment per 32-leaf group of the (ascending) items applies the leaf rule;
+    // groups whose argmax leaf decreased are recomputed from their leaves.
     const TreeGeom& geo = p.rgeo;
     Key* L1 = c.rtree + geo.off[1];
     int nrec = 0, ndirty = 0;
@@ -487,8 +533,8 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
       Key Q = L1[q];
       int I = c.ridx[q];
       const Key Q0 = Q;
-      bool rec = leaf_rule(Q, I, e_star, Num<T>::key(T(0)));
-      __syncwarp();
+      const bool rec = leaf_rule(Q, I, e_star, Num<T>::key(T(0)));
+      w.sync();
       if (lane == 0) {
         if (rec) c.dl1[nrec] = q;
         else {
@@ -499,16 +545,16 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
       }
       nrec += rec ? 1 : 0;
       ndirty += (rec || Q != Q0) ? 1 : 0;
-      __syncwarp();
+      w.sync();
     }
-    for (int base = 0; base < n_items; base += 32) {
+    for (int base = 0; base < n_items; base += G) {
       const int t = base + lane;
       const bool valid = t < n_items;
       const int e = valid ? c.items[t].x : -1;
       const int q = valid ? (e >> 5) : -1;
       const Key kk = valid ? c.nk[t] : Key(0);
       // lanes of one group form a contiguous segment (items ascend); reduce it
-      const unsigned peers = __match_any_sync(kFull, q);
+      const unsigned peers = w.match_any(q);
       const bool leader = valid && (__ffs(peers) - 1) == lane;
       Key Q = 0;
       int I = 0;
@@ -518,10 +564,10 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
       }
       // the group's argmax leaf decreased -> recompute from leaves
       const bool dec = valid && ((e == I && kk < Q) || p.dbg_full_tree);
-      const bool rec = __ballot_sync(kFull, dec) & peers;
+      const bool rec = (w.ballot(dec) & peers) != 0;
       // segment max of the new keys, lowest edge among ties
       int bi;
-      const Key km = warp_max_key_minidx_masked(kk, e, peers, &bi);
+      const Key km = warp_max_key_minidx_masked(kk, e, peers << w.base, &bi);
       bool changed = false;
       if (leader) {
         if (rec) changed = true;
@@ -532,27 +578,27 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
         }
       }
       const bool lrec = leader && rec;
-      const unsigned rb = __ballot_sync(kFull, lrec), cb = __ballot_sync(kFull, changed);
-      if (lrec) c.dl1[nrec + __popc(rb & lanemask_lt())] = q;
-      if (changed) c.dl0[ndirty + __popc(cb & lanemask_lt())] = q;
+      const unsigned rb = w.ballot(lrec), cb = w.ballot(changed);
+      if (lrec) c.dl1[nrec + __popc(rb & w.lt)] = q;
+      if (changed) c.dl0[ndirty + __popc(cb & w.lt)] = q;
       nrec += __popc(rb);
       ndirty += __popc(cb);
-      __syncwarp();
+      w.sync();
     }
-    auto rleaf = [&](int e) -> Key { return res_key<T, STORED>(c, e); };
-    for (int i = 0; i < nrec; ++i) group_recompute(c.rtree, c.ridx, geo, c.dl1[i], lane, rleaf);
-    __syncwarp();
-    if (geo.levels > 1) tree_fix_ancestors(c.rtree, geo, c.dl0, c.dl1, ndirty, lane, rleaf);
+    auto rleaf = [&](int e) -> Key { return res_key<T, STORED, G>(c, e); };
+    for (int i = 0; i < nrec; ++i) group_recompute(c.rtree, c.ridx, geo, c.dl1[i], w, rleaf);
+    w.sync();
+    if (geo.levels > 1) tree_fix_ancestors(c.rtree, geo, c.dl0, c.dl1, ndirty, w, rleaf);
   }
   if (CT) {  // incremental CI-tree update: n* first, then the two-hop VNs
     const TreeGeom& geo = p.cgeo;
     Key* L1 = c.ctree + geo.off[1];
-    int* se = (int*)c.stage;  // stage is free again: 32 (index, key) pairs
+    int* se = (int*)c.stage;  // stage is free again: G (index, key) pairs
     Key* sk = (Key*)(se + 32);
     int nrec = 0, ndirty = 0;
-    apply_leaf_updates(L1, c.cidx, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), lane, se, sk,
-                       c.dl1, nrec, c.dl0, ndirty);
-    for (int base = 0; base < n_items; base += 32) {
+    apply_leaf_updates(L1, c.cidx, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
+                       c.dl0, ndirty);
+    for (int base = 0; base < n_items; base += G) {
       const int t = base + lane;
       int j = -1;
       Key kk = 0;
@@ -560,12 +606,12 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
         j = g.edge_vn[c.items[t].x];
         kk = Num<T>::key(c.ci[j]);
       }
-      apply_leaf_updates(L1, c.cidx, j, kk, lane, se, sk, c.dl1, nrec, c.dl0, ndirty);
+      apply_leaf_updates(L1, c.cidx, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
     }
     auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
-    for (int i = 0; i < nrec; ++i) group_recompute(c.ctree, c.cidx, geo, c.dl1[i], lane, cleaf);
-    __syncwarp();
-    if (geo.levels > 1) tree_fix_ancestors(c.ctree, geo, c.dl0, c.dl1, ndirty, lane, cleaf);
+    for (int i = 0; i < nrec; ++i) group_recompute(c.ctree, c.cidx, geo, c.dl1[i], w, cleaf);
+    w.sync();
+    if (geo.levels > 1) tree_fix_ancestors(c.ctree, geo, c.dl0, c.dl1, ndirty, w, cleaf);
   }
   c.cnt[C_PROP] += 1;
   c.cnt[C_V2C] += vr.y - 1;
@@ -576,67 +622,68 @@ __device__ int propagate(const DynParams& p, Ctx<T>& c, int e_star) {
 
 // ------------------------------------------------------------ boundaries
 
-template <typename T>
-__device__ bool syndrome_ok(const DevGraph& g, const T* total, int lane) {  // E:179-188
-  for (int base = 0; base < g.M; base += 32) {
-    int m = base + lane;
+template <typename T, int G>
+__device__ bool syndrome_ok(const DevGraph& g, const T* total, const Grp<G>& w) {  // E:179-188
+  for (int base = 0; base < g.M; base += G) {
+    const int m = base + w.lane;
     int par = 0;
     if (m < g.M)
       for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e) par ^= (total[g.edge_vn[e]] < T(0)) ? 1 : 0;
-    if (__any_sync(kFull, par)) return false;
+    if (w.any(par)) return false;
   }
   return true;
 }
 
-template <typename T>
-__device__ void record_boundary(const DynParams& p, const T* total, long long f, int k, int lane) {
+template <typename T, int G>
+__device__ void record_boundary(const DynParams& p, const T* total, long long f, int k, const Grp<G>& w) {
   int errs = 0, ei = 0;
-  for (int n = lane; n < p.g.N; n += 32)
+  for (int n = w.lane; n < p.g.N; n += G)
     if (total[n] < T(0)) {
       ++errs;
       if (n < p.k_info) ++ei;
     }
-  errs = warp_sum(errs);
-  ei = warp_sum(ei);
-  if (lane == 0) {
+  errs = w.rsum(errs);
+  ei = w.rsum(ei);
+  if (w.lane == 0) {
     p.biterr[f * (p.i_max + 1) + k] = errs;
     p.biterr_info[f * (p.i_max + 1) + k] = ei;
   }
 }
 
-__device__ __forceinline__ void fill_remaining(const DynParams& p, long long f, int k, int lane) {
-  if (lane == 0)
+template <int G>
+__device__ __forceinline__ void fill_remaining(const DynParams& p, long long f, int k, const Grp<G>& w) {
+  if (w.lane == 0)
     for (int kk = k + 1; kk <= p.i_max; ++kk) {
       p.biterr[f * (p.i_max + 1) + kk] = p.biterr[f * (p.i_max + 1) + k];
       p.biterr_info[f * (p.i_max + 1) + kk] = p.biterr_info[f * (p.i_max + 1) + k];
     }
-  __syncwarp();
+  w.sync();
 }
 
 // single-edge boundary rule (E:377-384): returns true when decoding stops
-template <typename T>
-__device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T>& c, long long f, bool* conv) {
+template <typename T, int G>
+__device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c, long long f, bool* conv) {
   if (c.prop != c.next_b) return false;
   c.next_b += p.g.E;
-  int k = ++c.it;
-  record_boundary<T>(p, c.total, f, k, c.lane);
-  if (syndrome_ok<T>(p.g, c.total, c.lane)) {
+  const int k = ++c.it;
+  record_boundary<T, G>(p, c.total, f, k, c.w);
+  if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
     *conv = true;
-    fill_remaining(p, f, k, c.lane);
+    fill_remaining<G>(p, f, k, c.w);
     return true;
   }
   return false;
 }
 
 // multi-edge boundary rule (E:633-642)
-template <typename T>
-__device__ void me_boundaries(const DynParams& p, Ctx<T>& c, long long f, int* boundary, bool* conv) {
-  long long E = p.g.E;
+template <typename T, int G>
+__device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int* boundary, bool* conv) {
+  const long long E = p.g.E;
   while (*boundary <= p.i_max && c.prop >= (long long)(*boundary) * E) {
-    record_boundary<T>(p, c.total, f, *boundary, c.lane);
-    if (syndrome_ok<T>(p.g, c.total, c.lane)) {
+    record_boundary<T, G>(p, c.total, f, *boundary, c.w);
+    if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
       *conv = true;
-      fill_remaining(p, f, *boundary, c.lane);
+      fill_remaining<G>(p, f, *boundary, c.w);
     }
     ++(*boundary);
     if (*conv) break;
@@ -664,14 +711,14 @@ __device__ __forceinline__ int ci_group(T v, int n_g) {
 
 // Select up to n_p VNs (excluding n with excl[n] != 0 when excl != nullptr)
 // into out[0..count), ascending.  Reproduces _select_vns exactly.
-template <typename T>
-__device__ int select_vns(const DynParams& p, Ctx<T>& c, const uint8_t* excl, int n_p, int* out) {
+template <typename T, int G>
+__device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl, int n_p, int* out) {
   const int N = p.g.N, n_g = p.n_g, lane = c.lane;
-  for (int q = lane; q < n_g; q += 32) c.sizes[q] = 0;
-  __syncwarp();
-  for (int n = lane; n < N; n += 32)
+  for (int q = lane; q < n_g; q += G) c.sizes[q] = 0;
+  c.w.sync();
+  for (int n = lane; n < N; n += G)
     if (!excl || !excl[n]) atomicAdd(&c.sizes[ci_group(c.ci[n], n_g)], 1);
-  __syncwarp();
+  c.w.sync();
   int k_star = 0;
   if (lane == 0) {
     long long cum = 0;
@@ -681,28 +728,28 @@ __device__ int select_vns(const DynParams& p, Ctx<T>& c, const uint8_t* excl, in
       else break;
     }
   }
-  k_star = __shfl_sync(kFull, k_star, 0);
+  k_star = c.w.shfl(k_star, 0);
   const int thr = n_g - k_star;
   int count = 0;
-  for (int base = 0; base < N; base += 32) {
+  for (int base = 0; base < N; base += G) {
     int n = base + lane;
     bool s = n < N && (!excl || !excl[n]) && ci_group(c.ci[n], n_g) >= thr;
-    unsigned bal = __ballot_sync(kFull, s);
-    if (s) out[count + __popc(bal & lanemask_lt())] = n;
+    unsigned bal = c.w.ballot(s);
+    if (s) out[count + __popc(bal & c.w.lt)] = n;
     count += __popc(bal);
   }
-  __syncwarp();
+  c.w.sync();
   if (count < n_p && k_star < n_g) {
     const int fill = n_g - k_star - 1;
     int idx = 0;
-    for (int base = 0; base < N; base += 32) {
+    for (int base = 0; base < N; base += G) {
       int n = base + lane;
       bool s = n < N && (!excl || !excl[n]) && ci_group(c.ci[n], n_g) == fill;
-      unsigned bal = __ballot_sync(kFull, s);
-      if (s) c.members[idx + __popc(bal & lanemask_lt())] = n;
+      unsigned bal = c.w.ballot(s);
+      if (s) c.members[idx + __popc(bal & c.w.lt)] = n;
       idx += __popc(bal);
     }
-    __syncwarp();
+    c.w.sync();
     int need = n_p - count;
     if (need > idx) need = idx;
     if (lane == 0) {
@@ -716,43 +763,43 @@ __device__ int select_vns(const DynParams& p, Ctx<T>& c, const uint8_t* excl, in
       }
       c.rng = st;
     }
-    c.rng = __shfl_sync(kFull, c.rng, 0);
+    c.rng = c.w.shfl(c.rng, 0);
     count += need;
   }
-  __syncwarp();
+  c.w.sync();
   if (p.dump_buf && c.cur_f == 0 && lane == 0 && c.nsel < 8192)
     p.dump_buf[2 * N + c.nsel] = __longlong_as_double(c.rng);
   ++c.nsel;
   // ascending sort of out[0..count) (distinct VN ids): rank sort through members[]
-  for (int i = lane; i < count; i += 32) {
+  for (int i = lane; i < count; i += G) {
     int v = out[i], r = 0;
     for (int q = 0; q < count; ++q) r += out[q] < v;
     c.members[r] = v;
   }
-  __syncwarp();
-  for (int i = lane; i < count; i += 32) out[i] = c.members[i];
-  __syncwarp();
+  c.w.sync();
+  for (int i = lane; i < count; i += G) out[i] = c.members[i];
+  c.w.sync();
   return count;
 }
 
 // sort ints ascending in place (distinct values), via members[] scratch
-template <typename T>
-__device__ void sort_small(Ctx<T>& c, int* a, int count) {
-  for (int i = c.lane; i < count; i += 32) {
+template <typename T, int G>
+__device__ void sort_small(Ctx<T, G>& c, int* a, int count) {
+  for (int i = c.lane; i < count; i += G) {
     int v = a[i], r = 0;
     for (int q = 0; q < count; ++q) r += a[q] < v;
     c.members[r] = v;
   }
-  __syncwarp();
-  for (int i = c.lane; i < count; i += 32) a[i] = c.members[i];
-  __syncwarp();
+  c.w.sync();
+  for (int i = c.lane; i < count; i += G) a[i] = c.members[i];
+  c.w.sync();
 }
 
 // --------------------------------------------------------- local searches
 
 // E:436-469 after propagate(e_prev) left the item table of e_prev.
-template <typename T>
-__device__ int lmd_next_edge(const DynParams& p, Ctx<T>& c, int e_prev, int n_items, bool simplified) {
+template <typename T, int G>
+__device__ int lmd_next_edge(const DynParams& p, Ctx<T, G>& c, int e_prev, int n_items, bool simplified) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
   const int lane = c.lane;
@@ -763,26 +810,26 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T>& c, int e_prev, int n_it
   if (deg1) {
     int a = g.cn_ptr[mn.x], b = g.cn_ptr[mn.x + 1];
     ncand = b - a - 1;
-    for (int e = a + lane; e < b; e += 32)
+    for (int e = a + lane; e < b; e += G)
       if (e != e_prev) {
-        Key k = res_key<T, false>(c, e);
+        Key k = res_key<T, false, G>(c, e);
         if (k > bk) { bk = k; bi = e; }
       }
   } else {
     ncand = n_items;
-    for (int t = lane; t < n_items; t += 32) {
+    for (int t = lane; t < n_items; t += G) {
       int e = c.items[t].x;
-      Key k = res_key<T, false>(c, e);
+      Key k = res_key<T, false, G>(c, e);
       if (k > bk) { bk = k; bi = e; }
     }
   }
   if (ncand > 1) c.cnt[C_CMP] += ncand - 1;
   if (ncand <= 0) return -1;
   int best;
-  warp_max_key_minidx(bk, bi, &best);
+  c.w.max_key_minidx(bk, bi, &best);
   if (!simplified) {
     int np_ = g.edge_vn[best];
-    best = argmax_vn_edges<T>(g, c, np_, lane);
+    best = argmax_vn_edges<T, G>(g, c, np_);
     c.cnt[C_CMP] += g.vrec[np_].y - 1;
   }
   return best;
@@ -790,8 +837,8 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T>& c, int e_prev, int n_it
 
 // E:513-552: max-CI VN of the two-hop set of e_prev, ties -> lowest VN; the
 // candidate count (deduplicated, E:536-549) is precomputed per edge.
-template <typename T>
-__device__ int ci_argmax_twohop(const DynParams& p, Ctx<T>& c, int e_prev, int n_items, bool have_items) {
+template <typename T, int G>
+__device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, int n_items, bool have_items) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
   const int lane = c.lane;
@@ -802,16 +849,16 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T>& c, int e_prev, int n
   if (deg1) {
     int a = g.cn_ptr[mn.x], b = g.cn_ptr[mn.x + 1];
     ncand = b - a - 1;
-    for (int e = a + lane; e < b; e += 32)
+    for (int e = a + lane; e < b; e += G)
       if (e != e_prev) {
         int j = g.edge_vn[e];
         Key k = Num<T>::key(c.ci[j]);
         if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
       }
   } else {
-    if (!have_items) n_items = build_items<T>(g, c, e_prev);
+    if (!have_items) n_items = build_items<T, G>(g, c, e_prev);
     ncand = g.hop_distinct[e_prev];
-    for (int t = lane; t < n_items; t += 32) {
+    for (int t = lane; t < n_items; t += G) {
       int j = g.edge_vn[c.items[t].x];
       Key k = Num<T>::key(c.ci[j]);
       if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
@@ -820,33 +867,33 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T>& c, int e_prev, int n
   if (ncand > 1) c.cnt[C_CMP] += ncand - 1;
   if (ncand <= 0) return -1;
   int best;
-  warp_max_key_minidx(bk, bj, &best);
+  c.w.max_key_minidx(bk, bj, &best);
   return best;
 }
 
 // --------------------------------------------------------------- decoders
 
-template <typename T, int KERNEL, bool CI>
-__device__ void init_state(const DynParams& p, Ctx<T>& c, long long f) {  // E:106-127
+template <typename T, int KERNEL, bool CI, int G>
+__device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // E:106-127
   const DevGraph& g = p.g;
   const int lane = c.lane;
   const float* l32 = (const float*)p.llr + f * g.N;
   const double* l64 = (const double*)p.llr + f * g.N;
   auto chl = [&](int n) -> T { return p.llr_f64 ? (T)l64[n] : (T)l32[n]; };
-  for (int e = lane; e < g.E; e += 32) {
+  for (int e = lane; e < g.E; e += G) {
     T v = clampv(chl(g.edge_vn[e]));
     c.c2v[e] = T(0);
     c.in[e] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
   }
-  for (int n = lane; n < g.N; n += 32) c.total[n] = chl(n);
-  __syncwarp();
-  for (int m = lane; m < g.M; m += 32) {
+  for (int n = lane; n < g.N; n += G) c.total[n] = chl(n);
+  c.w.sync();
+  for (int m = lane; m < g.M; m += G) {
     int a = g.cn_ptr[m], b = g.cn_ptr[m + 1];
     for (int e = a; e < b; ++e) c.pre[e] = cn_msg_cached<T, KERNEL>(c.in, a, b, e);
   }
-  __syncwarp();
+  c.w.sync();
   if (CI)
-    for (int n = lane; n < g.N; n += 32) {
+    for (int n = lane; n < g.N; n += G) {
       T acc = chl(n);
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
       c.pretot[n] = acc;
@@ -855,12 +902,12 @@ __device__ void init_state(const DynParams& p, Ctx<T>& c, long long f) {  // E:1
       c.ci[n] = Num<T>::abs_(pt - p0(acc));
     }
   if (p.kind == KIND_ME_LMD_CIRBP)
-    for (int n = lane; n < g.N; n += 32) c.inpp[n] = 0;
-  __syncwarp();
+    for (int n = lane; n < g.N; n += G) c.inpp[n] = 0;
+  c.w.sync();
 }
 
-template <typename T, int KERNEL, int KF>
-__device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
+template <typename T, int KERNEL, int KF, int G>
+__device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
@@ -881,32 +928,32 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
   }
   const bool ci_kind = kind == KIND_CIRBP || kind == KIND_LMD_CIRBP || kind == KIND_ME_CIRBP ||
                        kind == KIND_ME_LMD_CIRBP;
-  if (ci_kind) init_state<T, KERNEL, true>(p, c, f);
-  else init_state<T, KERNEL, false>(p, c, f);
-  record_boundary<T>(p, c.total, f, 0, lane);
-  auto rleaf = [&](int e) -> Key { return res_key<T, false>(c, e); };
+  if (ci_kind) init_state<T, KERNEL, true, G>(p, c, f);
+  else init_state<T, KERNEL, false, G>(p, c, f);
+  record_boundary<T, G>(p, c.total, f, 0, c.w);
+  auto rleaf = [&](int e) -> Key { return res_key<T, false, G>(c, e); };
   auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
 
   switch (kind) {
     case KIND_RBP: {  // E:355-385
-      tree_build(c.rtree, c.ridx, p.rgeo, lane, rleaf);
+      tree_build(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
       while (c.prop < budget) {
-        int e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, rleaf);
+        int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
         c.cnt[C_CMP] += E - 1;
-        propagate<T, KERNEL, false, true, false, false>(p, c, e);
+        propagate<T, KERNEL, false, true, false, false, G>(p, c, e);
         ++c.prop;
-        if (single_boundary<T>(p, c, f, &conv)) break;
+        if (single_boundary<T, G>(p, c, f, &conv)) break;
       }
     } break;
     case KIND_CIRBP: {  // E:388-433
-      tree_build(c.rtree, c.ridx, p.rgeo, lane, rleaf);
+      tree_build(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
       const bool flat = p.flat_ci != 0;
-      if (!flat) tree_build(c.ctree, c.cidx, p.cgeo, lane, cleaf);
+      if (!flat) tree_build(c.ctree, c.cidx, p.cgeo, c.w, cleaf);
       const T gamma = (T)p.gamma;
       int kh = 0, kt = 0;  // per-iteration kappa tallies (warp-uniform)
       while (c.prop < budget) {
         const int it = c.it;
-        int n_star = flat ? argmax_scan<Key>(g.N, lane, cleaf) : tree_argmax(c.ctree, c.cidx, p.cgeo, lane, cleaf);
+        int n_star = flat ? argmax_scan<Key>(g.N, c.w, cleaf) : tree_argmax(c.ctree, c.cidx, p.cgeo, c.w, cleaf);
         c.cnt[C_CMP] += g.N - 1 + 1;
         c.cnt[C_KTRIALS] += 1;
         ++kt;
@@ -915,14 +962,14 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
         if (hit) {
           c.cnt[C_KHITS] += 1;
           ++kh;
-          e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, rleaf);
+          e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
           c.cnt[C_CMP] += E - 1;
         } else {
-          e = argmax_vn_edges<T>(g, c, n_star, lane);
+          e = argmax_vn_edges<T, G>(g, c, n_star);
           c.cnt[C_CMP] += g.vrec[n_star].y - 1;
         }
-        if (flat) propagate<T, KERNEL, true, true, false, false>(p, c, e);
-        else propagate<T, KERNEL, true, true, true, false>(p, c, e);
+        if (flat) propagate<T, KERNEL, true, true, false, false, G>(p, c, e);
+        else propagate<T, KERNEL, true, true, true, false, G>(p, c, e);
         ++c.prop;
         if (c.prop == c.next_b || c.prop >= budget) {
           if (lane == 0) {
@@ -931,82 +978,82 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
           }
           kh = kt = 0;
         }
-        if (single_boundary<T>(p, c, f, &conv)) break;
+        if (single_boundary<T, G>(p, c, f, &conv)) break;
       }
     } break;
     case KIND_LMDRBP:
     case KIND_SLMDRBP: {  // E:472-510
       const bool simplified = p.kind == KIND_SLMDRBP;  // sLMDRBP runs the LMDRBP kernel
-      int e = argmax_scan<Key>(g.E, lane, rleaf);
+      int e = argmax_scan<Key>(g.E, c.w, rleaf);
       c.cnt[C_CMP] += E - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, false, false, false, false>(p, c, e);
+        int n_items = propagate<T, KERNEL, false, false, false, false, G>(p, c, e);
         ++c.prop;
-        if (single_boundary<T>(p, c, f, &conv)) break;
+        if (single_boundary<T, G>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
-        int en = lmd_next_edge<T>(p, c, e, n_items, simplified);
+        int en = lmd_next_edge<T, G>(p, c, e, n_items, simplified);
         if (en < 0) {
-          en = argmax_scan<Key>(g.E, lane, rleaf);
+          en = argmax_scan<Key>(g.E, c.w, rleaf);
           c.cnt[C_CMP] += E - 1;
         }
         e = en;
       }
     } break;
     case KIND_LMD_CIRBP: {  // E:555-598
-      int n_star = argmax_scan<Key>(g.N, lane, cleaf);
+      int n_star = argmax_scan<Key>(g.N, c.w, cleaf);
       c.cnt[C_CMP] += g.N - 1;
-      int e = argmax_vn_edges<T>(g, c, n_star, lane);
+      int e = argmax_vn_edges<T, G>(g, c, n_star);
       c.cnt[C_CMP] += g.vrec[n_star].y - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, true, false, false, false>(p, c, e);
+        int n_items = propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
         ++c.prop;
-        if (single_boundary<T>(p, c, f, &conv)) break;
+        if (single_boundary<T, G>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
-        int nn = ci_argmax_twohop<T>(p, c, e, n_items, true);
+        int nn = ci_argmax_twohop<T, G>(p, c, e, n_items, true);
         if (nn < 0) {
-          nn = argmax_scan<Key>(g.N, lane, cleaf);
+          nn = argmax_scan<Key>(g.N, c.w, cleaf);
           c.cnt[C_CMP] += g.N - 1;
         }
-        e = argmax_vn_edges<T>(g, c, nn, lane);
+        e = argmax_vn_edges<T, G>(g, c, nn);
         c.cnt[C_CMP] += g.vrec[nn].y - 1;
       }
     } break;
     case KIND_ME_CIRBP: {  // E:601-643
       int boundary = 1;
       while (boundary <= I && !conv) {
-        int count = select_vns<T>(p, c, nullptr, p.n_p, c.sel);
+        int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
         c.cnt[C_MSEL] += p.n_g;
         for (int idx = 0; idx < count; ++idx) {
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T>(g, c, pv, lane);
+          int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
-          propagate<T, KERNEL, true, false, false, false>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
           ++c.prop;
         }
-        me_boundaries<T>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G>(p, c, f, &boundary, &conv);
       }
     } break;
     case KIND_ME_LMD_CIRBP: {  // E:646-716
       int boundary = 1;
-      int count = select_vns<T>(p, c, nullptr, p.n_p, c.sel);
+      int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
       c.cnt[C_MSEL] += p.n_g;
       while (boundary <= I && !conv) {
         for (int idx = 0; idx < count; ++idx) {
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T>(g, c, pv, lane);
+          int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
           if (lane == 0) c.chosen[idx] = e;
-          propagate<T, KERNEL, true, false, false, false>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
           ++c.prop;
         }
-        me_boundaries<T>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G>(p, c, f, &boundary, &conv);
         if (conv || boundary > I) break;
         // P' = two-hop max-CI VN of each chosen edge, deduplicated in order
         int npc = 0;
         for (int idx = 0; idx < count; ++idx) {
-          int pn = ci_argmax_twohop<T>(p, c, c.chosen[idx], 0, false);
+          int pn = ci_argmax_twohop<T, G>(p, c, c.chosen[idx], 0, false);
           bool add = pn >= 0 && !c.inpp[pn];
-          __syncwarp();
+          c.w.sync();
           if (add) {
             if (lane == 0) {
               c.inpp[pn] = 1;
@@ -1014,59 +1061,59 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
             }
             ++npc;
           }
-          __syncwarp();
+          c.w.sync();
         }
         if (npc < p.n_p) {
-          int extra = select_vns<T>(p, c, c.inpp, p.n_p - npc, c.sel + npc);
+          int extra = select_vns<T, G>(p, c, c.inpp, p.n_p - npc, c.sel + npc);
           c.cnt[C_MSEL] += p.n_g;
           count = npc + extra;
         } else {
           count = npc;
         }
-        for (int idx = lane; idx < npc; idx += 32) c.inpp[c.sel[idx]] = 0;
-        __syncwarp();
-        sort_small<T>(c, c.sel, count);
+        for (int idx = lane; idx < npc; idx += G) c.inpp[c.sel[idx]] = 0;
+        c.w.sync();
+        sort_small<T, G>(c, c.sel, count);
       }
     } break;
     case KIND_ME_RBP: {  // new (oracle/ldpc_oracle.c decode_me_rbp): stored residuals
-      for (int e = lane; e < g.E; e += 32) c.res[e] = Num<T>::abs_(c.pre[e] - c.c2v[e]);
-      __syncwarp();
-      auto sleaf = [&](int e) -> Key { return res_key<T, true>(c, e); };
-      tree_build(c.rtree, c.ridx, p.rgeo, lane, sleaf);
+      for (int e = lane; e < g.E; e += G) c.res[e] = Num<T>::abs_(c.pre[e] - c.c2v[e]);
+      c.w.sync();
+      auto sleaf = [&](int e) -> Key { return res_key<T, true, G>(c, e); };
+      tree_build(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
       int boundary = 1;
       const int np_ = p.n_p < g.E ? p.n_p : g.E;
       while (boundary <= I && !conv) {
         for (int t = 0; t < np_; ++t) {
-          int e = tree_argmax(c.rtree, c.ridx, p.rgeo, lane, sleaf);
+          int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
           if (lane == 0) {
             c.sel[t] = e;
             c.tmp[t] = c.res[e];
             c.res[e] = T(-1);  // excluded: key 0
             c.dl0[0] = e >> 5;
           }
-          __syncwarp();
-          tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, 1, lane, sleaf);
+          c.w.sync();
+          tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, 1, c.w, sleaf);
         }
-        for (int t = lane; t < np_; t += 32) {
+        for (int t = lane; t < np_; t += G) {
           c.res[c.sel[t]] = c.tmp[t];
           c.dl0[t] = c.sel[t] >> 5;
         }
-        __syncwarp();
-        tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, np_, lane, sleaf);
+        c.w.sync();
+        tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, np_, c.w, sleaf);
         c.cnt[C_CMP] += E - 1;
-        sort_small<T>(c, c.sel, np_);
+        sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
-          propagate<T, KERNEL, false, true, false, true>(p, c, c.sel[idx]);
+          propagate<T, KERNEL, false, true, false, true, G>(p, c, c.sel[idx]);
           ++c.prop;
         }
-        me_boundaries<T>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G>(p, c, f, &boundary, &conv);
       }
     } break;
     default:
       break;
   }
-  if (I == 0) conv = syndrome_ok<T>(g, c.total, lane);  // schedules.py:144-146
-  for (int n = lane; n < g.N; n += 32) p.u_hat[f * g.N + n] = c.total[n] < T(0) ? 1 : 0;
+  if (I == 0) conv = syndrome_ok<T, G>(g, c.total, c.w);  // schedules.py:144-146
+  for (int n = lane; n < g.N; n += G) p.u_hat[f * g.N + n] = c.total[n] < T(0) ? 1 : 0;
   if (lane < kCounters) {
     long long v = 0;
 #pragma unroll
@@ -1078,29 +1125,33 @@ __device__ void decode_frame(const DynParams& p, Ctx<T>& c, long long f) {
     p.prop[f] = c.prop;
     p.conv[f] = conv ? 1 : 0;
   }
-  __syncwarp();
+  c.w.sync();
 }
 
 // MODE 0: E, N and T parts in shared memory; 1: E in HBM, N and T in shared;
-// 2: E and N in HBM, T in shared; 3: everything in HBM.
-template <typename T, int KERNEL, int MODE, int KF>
+// 2: E and N in HBM, T in shared; 3: everything in HBM.  G lanes per frame
+// (32/G frames per warp); slots and scratch are per frame.
+template <typename T, int KERNEL, int MODE, int KF, int G>
 __global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  const long long gw = (long long)blockIdx.x * wpb + warp;
+  constexpr int FPW = 32 / G;  // frames per warp
+  const int fpb = (blockDim.x >> 5) * FPW;
+  const int fr = (threadIdx.x >> 5) * FPW + (threadIdx.x & 31) / G;  // frame slot in the block
+  const long long gf = (long long)blockIdx.x * fpb + fr;
   const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes;
-  // shared bytes per warp and HBM bytes per warp for this mode
+  // shared bytes per frame and HBM bytes per frame for this mode
   const long long sh = (MODE == 0 ? sE + sN + sT : MODE == 1 ? sN + sT : MODE == 2 ? sT : 0);
   const long long hb = (MODE == 0 ? 0 : MODE == 1 ? sE : MODE == 2 ? sE + sN : sE + sN + sT);
-  unsigned char* shw = smem + warp * sh;
-  unsigned char* hbw = p.ws + gw * hb;
+  unsigned char* shw = smem + fr * sh;
+  unsigned char* hbw = p.ws + gf * hb;
   unsigned char* bE = MODE == 0 ? shw : hbw;
   unsigned char* bN = MODE == 0 ? shw + sE : MODE == 1 ? shw : hbw + sE;
   unsigned char* bT = MODE == 0 ? shw + sE + sN : MODE == 1 ? shw + sN : MODE == 2 ? shw : hbw + sE + sN;
-  unsigned char* scr = smem + (long long)wpb * sh + (long long)warp * p.scratch_bytes;
+  unsigned char* scr = smem + (long long)fpb * sh + (long long)fr * p.scratch_bytes;
   using Key = typename Num<T>::Key;
-  Ctx<T> c;
-  c.lane = threadIdx.x & 31;
+  Ctx<T, G> c;
+  c.w = Grp<G>::make();
+  c.lane = c.w.lane;
   c.c2v = (T*)(bE + p.o_c2v);
   c.pre = (T*)(bE + p.o_pre);
   c.in = (T*)(bE + p.o_in);
@@ -1128,9 +1179,9 @@ __global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(co
   for (;;) {
     unsigned long long f = 0;
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);
-    f = __shfl_sync(kFull, f, 0);
+    f = c.w.shfl(f, 0);
     if ((long long)f >= p.B) break;
-    decode_frame<T, KERNEL, KF>(p, c, (long long)f);
+    decode_frame<T, KERNEL, KF, G>(p, c, (long long)f);
   }
 }
 

@@ -1,19 +1,25 @@
-// Dynamic-schedule kernels: double state, KERNEL_EXACT; instantiated per (placement mode, kind).
+// Dynamic-schedule kernels: double state, KERNEL_EXACT; per (placement mode, kind, lanes per frame).
 #include "dyn_engine.cuh"
 #include "kernel_table.h"
 using namespace ldpc;
-void* dyn_f64_exact_c_get(int mode, int kind) {
-  if (kind == KIND_ME_CIRBP || KIND_ME_CIRBP < 0) switch (mode) {
-      case 0: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 0, KIND_ME_CIRBP>;
-      case 1: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 1, KIND_ME_CIRBP>;
-      case 2: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 2, KIND_ME_CIRBP>;
-      case 3: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 3, KIND_ME_CIRBP>;
+void* dyn_f64_exact_c_get(int mode, int kind, int g16) {
+  if (kind == KIND_LMDRBP) {
+    if (g16) return nullptr;  // 16-lane groups measured slower (halves diverge); not built
+    switch (mode) {
+      case 0: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 0, KIND_LMDRBP, 32>;
+      case 1: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 1, KIND_LMDRBP, 32>;
+      case 2: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 2, KIND_LMDRBP, 32>;
+      case 3: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 3, KIND_LMDRBP, 32>;
     }
-  if (kind == KIND_ME_LMD_CIRBP || KIND_ME_LMD_CIRBP < 0) switch (mode) {
-      case 0: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 0, KIND_ME_LMD_CIRBP>;
-      case 1: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 1, KIND_ME_LMD_CIRBP>;
-      case 2: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 2, KIND_ME_LMD_CIRBP>;
-      case 3: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 3, KIND_ME_LMD_CIRBP>;
+  }
+  if (kind == KIND_LMD_CIRBP) {
+    if (g16) return nullptr;  // 16-lane groups measured slower (halves diverge); not built
+    switch (mode) {
+      case 0: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 0, KIND_LMD_CIRBP, 32>;
+      case 1: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 1, KIND_LMD_CIRBP, 32>;
+      case 2: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 2, KIND_LMD_CIRBP, 32>;
+      case 3: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 3, KIND_LMD_CIRBP, 32>;
     }
+  }
   return nullptr;
 }

@@ -80,7 +80,8 @@ int smem_optin() {
 
 struct DynPlan {
   DynParams p;
-  int mode;  // 0: all smem, 1: per-edge part in HBM, 2: all HBM
+  int mode;  // 0: all smem, 1: E part in HBM, 2: E+N parts in HBM, 3: all HBM
+  int g16;   // 16 lanes per frame (2 frames per warp)
   int warps_per_block;
   int blocks;
   long long ws_bytes;  // including the 256-byte header (work counter)
@@ -152,8 +153,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
 }
 
 template <typename T>
-void* pick_dyn_kernel(int kernel, int mode, int kind) {
-  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind);
+void* pick_dyn_kernel(int kernel, int mode, int kind, int g16) {
+  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind, g16);
 }
 
 template <typename T>
@@ -176,54 +177,62 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
   dyn_layout<T>(G, s, p);
   const long long optin = smem_optin() - 1024;
   const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes, sc = p.scratch_bytes;
-  const long long sh[4] = {sE + sN + sT + sc, sN + sT + sc, sT + sc, sc};
-  const long long hb[4] = {0, sE, sE + sN, sE + sN + sT};
-  struct Cand { int mode, wpb; long long smem; int occ; };
-  auto make = [&](int mode) {
-    Cand c{mode, 0, 0, 0};
-    const long long per = sh[mode];
+  const long long sh[4] = {sE + sN + sT + sc, sN + sT + sc, sT + sc, sc};  // shared bytes per frame
+  const long long hb[4] = {0, sE, sE + sN, sE + sN + sT};                 // HBM bytes per frame
+  struct Cand { int mode, g16, wpb; long long smem; int occ; long long frames; };
+  const char* lanes_env = getenv("LDPC_LANES");
+  const int lanes_force = lanes_env ? atoi(lanes_env) : 0;
+  auto make = [&](int mode, int g16) {
+    Cand c{mode, g16, 0, 0, 0, 0};
+    const int fpw = g16 ? 2 : 1;
+    const long long per = sh[mode] * fpw;  // shared bytes per warp
     if (per > optin) return c;
-    int w = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / per);
+    void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16);
+    if (!fn) return c;
+    int w = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / std::max<long long>(per, 1));
     c.wpb = std::max(1, w);
     c.smem = per * c.wpb;
-    c.occ = dyn_occupancy<T>(pick_dyn_kernel<T>(s->kernel, mode, s->kind), c.wpb, (int)c.smem);
+    c.occ = dyn_occupancy<T>(fn, c.wpb, (int)c.smem);
+    c.frames = std::min<long long>((long long)c.occ * c.wpb * fpw * sm_count(), B);
     return c;
   };
-  Cand cands[4] = {make(0), make(1), make(2), make(3)};
-  auto warps = [](const Cand& c) { return (long long)c.occ * c.wpb; };
-  Cand ch{-1, 0, 0, 0};
-  if (s->placement == 1) ch = cands[3];
-  else if (s->placement == 2) ch = cands[1];
-  else if (s->placement == 3) ch = cands[0];
-  else if (s->placement == 4) ch = cands[2];
-  else {
-    // The update chain is latency-bound, so resident frames decide throughput
-    // (measured on C0-C2: split/trees placements with 16-24 warps/SM beat the
-    // all-shared 3-5 warps/SM by ~2x even when the per-edge part spills past
-    // L2).  Most resident frames wins; within 10% the more on-chip mode wins.
-    long long best = 0;
-    for (int m = 0; m < 4; ++m)
-      if (cands[m].occ > 0) best = std::max(best, std::min<long long>(warps(cands[m]) * sm_count(), B));
-    for (int m = 0; m < 4 && ch.mode < 0; ++m) {
-      const Cand& c = cands[m];
-      if (c.occ <= 0) continue;
-      const long long frames = std::min<long long>(warps(c) * sm_count(), B);
-      if (frames * 10 >= best * 9) ch = c;
+  std::vector<Cand> cands;
+  for (int m = 0; m < 4; ++m)
+    for (int g16 = 0; g16 < 2; ++g16) {
+      if (lanes_force == 16 && !g16) continue;
+      if (lanes_force == 32 && g16) continue;
+      Cand c = make(m, g16);
+      if (c.occ > 0) cands.push_back(c);
     }
-  }
+  const int want_mode = s->placement == 1 ? 3 : s->placement == 2 ? 1 : s->placement == 3 ? 0
+                        : s->placement == 4 ? 2 : -1;
+  Cand ch{-1, 0, 0, 0, 0, 0};
+  // The update chain is latency-bound, so resident frames decide throughput
+  // (measured on C0-C2).  Most resident frames wins; within 10% the more
+  // on-chip mode, then 32 lanes per frame, wins.
+  long long best = 0;
+  for (auto& c : cands)
+    if (want_mode < 0 || c.mode == want_mode) best = std::max(best, c.frames);
+  for (int m = 0; m < 4 && ch.mode < 0; ++m)
+    for (int g16 = 0; g16 < 2 && ch.mode < 0; ++g16)
+      for (auto& c : cands)
+        if (c.mode == m && c.g16 == g16 && (want_mode < 0 || m == want_mode) && c.frames * 10 >= best * 9) ch = c;
   if (ch.mode < 0 || ch.occ <= 0) return LDPC_ERR_UNSUPPORTED;
   pl.mode = ch.mode;
+  pl.g16 = ch.g16;
   pl.warps_per_block = ch.wpb;
   pl.smem_bytes = (int)ch.smem;
+  const int fpw = ch.g16 ? 2 : 1;
   long long blocks = (long long)ch.occ * sm_count();
-  long long max_warps = B;
-  if (s->max_resident > 0) max_warps = std::min<long long>(max_warps, s->max_resident);
-  const long long hbm_per_warp = hb[ch.mode];
-  if (hbm_per_warp > 0) max_warps = std::min(max_warps, std::max<long long>(1, (24ll << 30) / hbm_per_warp));
-  long long need_blocks = (max_warps + pl.warps_per_block - 1) / pl.warps_per_block;
+  long long max_frames = B;
+  if (s->max_resident > 0) max_frames = std::min<long long>(max_frames, s->max_resident);
+  const long long hbm_per_frame = hb[ch.mode];
+  if (hbm_per_frame > 0) max_frames = std::min(max_frames, std::max<long long>(1, (24ll << 30) / hbm_per_frame));
+  const long long fpb = (long long)pl.warps_per_block * fpw;
+  long long need_blocks = (max_frames + fpb - 1) / fpb;
   blocks = std::max<long long>(1, std::min(blocks, need_blocks));
   pl.blocks = (int)blocks;
-  pl.ws_bytes = 256 + blocks * pl.warps_per_block * hbm_per_warp;
+  pl.ws_bytes = 256 + blocks * fpb * hbm_per_frame;
   return LDPC_OK;
 }
 
@@ -324,7 +333,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.log_cap = g_log_cap;
     p.ws = (unsigned char*)ws + 256;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
-    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind);
+    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16);
     void* args[] = {&p};
     if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,
                                              pl.smem_bytes, st)))
@@ -367,9 +376,10 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
 __global__ void select_vns_kernel(const double* ci, const uint8_t* mask, int N, int n_g, int n_p,
                                   long long seed, int* out, int* count_out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Ctx<double> c;
+  Ctx<double, 32> c;
   memset(&c, 0, sizeof(c));
-  c.lane = threadIdx.x & 31;
+  c.w = Grp<32>::make();
+  c.lane = c.w.lane;
   c.ci = const_cast<double*>(ci);
   c.sizes = (int*)smem;
   c.members = (int*)(smem + align16((long long)n_g * 4));
@@ -381,7 +391,7 @@ __global__ void select_vns_kernel(const double* ci, const uint8_t* mask, int N, 
   memset(&p, 0, sizeof(p));
   p.g.N = N;
   p.n_g = n_g;
-  int cnt = select_vns<double>(p, c, excl, n_p, out);
+  int cnt = select_vns<double, 32>(p, c, excl, n_p, out);
   if (c.lane == 0) *count_out = cnt;
 }
 

@@ -225,4 +225,80 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
+// ------------------------------------------------------------ lane groups
+// A frame is decoded by a group of G lanes (G = 32: one warp; G = 16: two
+// frames per warp).  All collectives use the group's mask, so the two halves
+// of a warp may diverge freely (independent thread scheduling interleaves them).
+template <int G>
+struct Grp {
+  static constexpr int kG = G;
+  unsigned mask;  // warp-level mask of this group's lanes
+  int base;       // first warp lane of the group
+  int lane;       // lane within the group
+  unsigned lt;    // group-local mask of lower lanes
+  __device__ __forceinline__ static Grp make() {
+    Grp g;
+    const int wl = threadIdx.x & 31;
+    g.base = G == 32 ? 0 : (wl / G) * G;
+    g.lane = wl - g.base;
+    g.mask = G == 32 ? kFull : (((1u << G) - 1u) << g.base);
+    g.lt = (1u << g.lane) - 1u;
+    return g;
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <typename V> __device__ __forceinline__ V shfl(V v, int src) const {
+    return __shfl_sync(mask, v, base + src);
+  }
+  template <typename V> __device__ __forceinline__ V shfl_up(V v, int d) const {
+    return __shfl_up_sync(mask, v, d, G);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask, p) >> base; }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  __device__ __forceinline__ unsigned match_any(int v) const { return __match_any_sync(mask, v) >> base; }
+  __device__ __forceinline__ unsigned rmax(unsigned v) const { return __reduce_max_sync(mask, v); }
+  __device__ __forceinline__ unsigned rmin(unsigned v) const { return __reduce_min_sync(mask, v); }
+  __device__ __forceinline__ int rsum(int v) const { return (int)__reduce_add_sync(mask, (unsigned)v); }
+  __device__ __forceinline__ int incl_scan(int v) const {
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      int t = __shfl_up_sync(mask, v, d, G);
+      if (lane >= d) v += t;
+    }
+    return v;
+  }
+  // max key (lowest lane among ties); returns group lane of the winner
+  __device__ __forceinline__ unsigned long long max_key(unsigned long long k, int* ln) const {
+    unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+    unsigned mh = rmax(hi);
+    unsigned ml = rmax(hi == mh ? lo : 0u);
+    *ln = __ffs(ballot(hi == mh && lo == ml)) - 1;
+    return ((unsigned long long)mh << 32) | ml;
+  }
+  __device__ __forceinline__ unsigned max_key(unsigned k, int* ln) const {
+    unsigned m = rmax(k);
+    *ln = __ffs(ballot(k == m)) - 1;
+    return m;
+  }
+  __device__ __forceinline__ unsigned long long max_key_only(unsigned long long k) const {
+    unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+    unsigned mh = rmax(hi);
+    unsigned ml = rmax(hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+  }
+  __device__ __forceinline__ unsigned max_key_only(unsigned k) const { return rmax(k); }
+  // max key with the smallest companion index among ties
+  __device__ __forceinline__ unsigned long long max_key_minidx(unsigned long long k, int idx, int* out) const {
+    unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+    unsigned mh = rmax(hi);
+    unsigned ml = rmax(hi == mh ? lo : 0u);
+    *out = (int)rmin((hi == mh && lo == ml) ? (unsigned)idx : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
+  }
+  __device__ __forceinline__ unsigned max_key_minidx(unsigned k, int idx, int* out) const {
+    unsigned m = rmax(k);
+    *out = (int)rmin(k == m ? (unsigned)idx : 0xffffffffu);
+    return m;
+  }
+};
+
 }  // namespace ldpc

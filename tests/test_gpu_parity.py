@@ -148,3 +148,30 @@ def test_fp32_mode_statistics():
     fb = (b["bit_errors_at"][:, -1] > 0).mean()
     assert abs(fa - fb) < 4 * np.sqrt(fa * (1 - fa) / len(llrs)) + 1e-3
     assert ((a["u_hat"] == b["u_hat"]).all(1)).mean() > 0.95
+
+
+def test_device_frame_generation_statistics():
+    """On-GPU BPSK-AWGN frames: LLR moments match 2/s^2, 4/s^2; punctured = 0;
+    decoding them gives a FER inside the host-generated frames' 99% CI."""
+    from paper_2102_11089_b200.channel import ebn0_to_sigma, llr_batch_device
+    spec, g = load_code("C2")
+    B = 4096
+    llr = llr_batch_device(spec, 1.0, seed=7, start=0, count=B, dtype=torch.float64).cpu().numpy()
+    s = ebn0_to_sigma(1.0, spec)
+    p = len(spec.punctured)
+    assert (llr[:, :p] == 0).all()
+    tx = llr[:, p:]
+    unclipped = tx[np.abs(tx) < 30]
+    assert abs(tx.mean() - 2 / s**2) < 0.01 * (2 / s**2)
+    assert abs(unclipped.std() - 2 / s) < 0.02 * (2 / s)
+    # deterministic per (seed, frame): a sub-range reproduces the same rows
+    again = llr_batch_device(spec, 1.0, seed=7, start=100, count=10, dtype=torch.float64).cpu().numpy()
+    np.testing.assert_array_equal(again, llr[100:110])
+    # FER agreement with host frames (flooding, C0)
+    spec0, g0 = load_code("C0")
+    cfg = _cfg({"kind": "flooding", "i_max": 5})
+    dev = _gpu(spec0, llr_batch_device(spec0, 2.0, seed=0, start=0, count=20000).cpu().numpy(), cfg)
+    host = _gpu(spec0, llr_batch(spec0, 2.0, seed=0, start=0, count=20000), cfg)
+    fd = (dev["bit_errors_at"][:, -1] > 0).mean()
+    fh = (host["bit_errors_at"][:, -1] > 0).mean()
+    assert abs(fd - fh) < 2.58 * np.sqrt(2 * fh * (1 - fh) / 20000) + 1e-3
