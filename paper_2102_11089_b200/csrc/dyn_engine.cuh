@@ -69,12 +69,13 @@ struct DynParams {
   unsigned char* ws;      // HBM slots
   long long slotE_bytes, slotN_bytes, slotT_bytes;
   long long o_c2v, o_pre, o_in, o_res;                           // E part
-  long long o_total, o_pretot, o_ci, o_p0t, o_inpp, o_members, o_sel, o_chosen, o_tmp;  // N part
+  long long o_total, o_pretot, o_ci, o_p0t, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
   long long o_rtree, o_ridx, o_ctree, o_cidx;                    // T part
   TreeGeom rgeo, cgeo;
   int flat_ci;            // CIRBP: flat CI argmax instead of a tree
   int scratch_bytes;      // per-warp shared scratch
-  int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes;
+  int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes, so_hist;
+  int fast_sel;           // ME kinds with n_g <= 255: maintained groups + histogram
 };
 
 template <typename T, int G>
@@ -85,6 +86,9 @@ struct Ctx {
   Key *rtree, *ctree;  // tree node keys, all levels
   int *ridx, *cidx;    // level-1 argmax leaf of each 32-leaf group
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
+  uint8_t* gid;   // ME kinds: Alg.-4 group of each VN (maintained)
+  int* hist;      // ME kinds: VNs per group (maintained)
+  unsigned* gbits;  // ME kinds: membership bitmap of each group (maintained)
   int *members, *sel, *chosen;
   const int4* items;  // two-hop edges of the last update (g, a, d, stage base), ascending g
   int4* items_buf;    // per-warp scratch for items built on the fly
@@ -374,12 +378,34 @@ __device__ int build_items(const DevGraph& g, Ctx<T, G>& c, int e_star) {
   return n;
 }
 
+template <typename T>
+__device__ __forceinline__ int ci_group(T v, int n_g) {
+  int gi = (int)(v * (T)n_g);
+  return gi > n_g - 1 ? n_g - 1 : gi;
+}
+
+// Alg.-4 group of a VN whose CI was just written (E:304-307), kept with the
+// group-size histogram and one membership bitmap per group (n_g x W words,
+// W = ceil(N/32)), so a selection round reads k*+1 bitmap rows, not N CIs.
+template <typename T, int G>
+__device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int j, T v) {
+  const int gn = ci_group(v, n_g), go = c.gid[j];
+  if (gn != go) {
+    atomicSub(&c.hist[go], 1);
+    atomicAdd(&c.hist[gn], 1);
+    const unsigned bit = 1u << (j & 31);
+    atomicAnd(&c.gbits[go * W + (j >> 5)], ~bit);
+    atomicOr(&c.gbits[gn * W + (j >> 5)], bit);
+    c.gid[j] = (uint8_t)gn;
+  }
+}
+
 // ------------------------------------------------------------- propagate
 
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
 // pre-C2V (and, for CI schedules, pre_total / CI) state.  Leaves the item
 // table of e* for the LMD searches.
-template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G>
+template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G, bool MG = false>
 __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
@@ -418,7 +444,9 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     if (CI) {
       const T pt = p0(tot);  // cached p0(total) of n*, the only total that changes
       c.p0t[n_star] = pt;
-      c.ci[n_star] = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
+      const T cv = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
+      c.ci[n_star] = cv;
+      if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
     }
   }
   // V2C to the other checks of n* (E:153-160), also staged; slots in chunks of G
@@ -504,7 +532,9 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (valid) {
           T pt = c.pretot[j] + delta;  // E:171
           c.pretot[j] = pt;
-          c.ci[j] = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
+          const T cv = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
+          c.ci[j] = cv;
+          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
         }
       } else {
         // the same VN reached through two checks (4-cycle): keep the reference's order
@@ -516,7 +546,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           w.sync();
         }
         const bool last = valid && ((peers >> lane) >> 1) == 0;
-        if (last) c.ci[j] = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
+        if (last) {
+          const T cv = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
+          c.ci[j] = cv;
+          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+        }
       }
     }
   }
@@ -613,6 +647,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     w.sync();
     if (geo.levels > 1) tree_fix_ancestors(c.ctree, geo, c.dl0, c.dl1, ndirty, w, cleaf);
   }
+  if (MG && p.fast_sel) w.sync();
   c.cnt[C_PROP] += 1;
   c.cnt[C_V2C] += vr.y - 1;
   c.cnt[C_PRE] += n_items;
@@ -703,56 +738,49 @@ __device__ __forceinline__ long long rand_next(long long* st) {
   return z;
 }
 
-template <typename T>
-__device__ __forceinline__ int ci_group(T v, int n_g) {
-  int gi = (int)(v * (T)n_g);
-  return gi > n_g - 1 ? n_g - 1 : gi;
-}
 
 // Select up to n_p VNs (excluding n with excl[n] != 0 when excl != nullptr)
 // into out[0..count), ascending.  Reproduces _select_vns exactly.
+// k* of Alg. 4 from a group-size histogram: the largest k with
+// sum_{q >= n_g-k} size[q] <= n_p (E:308-314); *sel_total = that sum.
 template <typename T, int G>
-__device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl, int n_p, int* out) {
-  const int N = p.g.N, n_g = p.n_g, lane = c.lane;
-  for (int q = lane; q < n_g; q += G) c.sizes[q] = 0;
-  c.w.sync();
-  for (int n = lane; n < N; n += G)
-    if (!excl || !excl[n]) atomicAdd(&c.sizes[ci_group(c.ci[n], n_g)], 1);
-  c.w.sync();
-  int k_star = 0;
-  if (lane == 0) {
-    long long cum = 0;
-    for (int k = 1; k <= n_g; ++k) {
-      cum += c.sizes[n_g - k];
-      if (cum <= n_p) k_star = k;
-      else break;
+__device__ __forceinline__ int kstar_of(Ctx<T, G>& c, const int* hist, int n_g, int n_p, int* sel_total) {
+  int k_star = 0, tot = 0;
+  if (n_g <= G) {
+    const int v = c.lane < n_g ? hist[n_g - 1 - c.lane] : 0;
+    const int cum = c.w.incl_scan(v);
+    k_star = __popc(c.w.ballot(c.lane < n_g && cum <= n_p));
+    tot = c.w.shfl(cum, k_star > 0 ? k_star - 1 : 0);
+    if (k_star == 0) tot = 0;
+  } else {
+    if (c.lane == 0) {
+      long long cum = 0;
+      for (int k = 1; k <= n_g; ++k) {
+        cum += hist[n_g - k];
+        if (cum <= n_p) {
+          k_star = k;
+          tot = (int)cum;
+        } else {
+          break;
+        }
+      }
     }
+    k_star = c.w.shfl(k_star, 0);
+    tot = c.w.shfl(tot, 0);
   }
-  k_star = c.w.shfl(k_star, 0);
-  const int thr = n_g - k_star;
-  int count = 0;
-  for (int base = 0; base < N; base += G) {
-    int n = base + lane;
-    bool s = n < N && (!excl || !excl[n]) && ci_group(c.ci[n], n_g) >= thr;
-    unsigned bal = c.w.ballot(s);
-    if (s) out[count + __popc(bal & c.w.lt)] = n;
-    count += __popc(bal);
-  }
-  c.w.sync();
-  if (count < n_p && k_star < n_g) {
-    const int fill = n_g - k_star - 1;
-    int idx = 0;
-    for (int base = 0; base < N; base += G) {
-      int n = base + lane;
-      bool s = n < N && (!excl || !excl[n]) && ci_group(c.ci[n], n_g) == fill;
-      unsigned bal = c.w.ballot(s);
-      if (s) c.members[idx + __popc(bal & c.w.lt)] = n;
-      idx += __popc(bal);
-    }
-    c.w.sync();
+  *sel_total = tot;
+  return k_star;
+}
+
+// Alg.-4 tail shared by the selection variants: random fill from the next
+// group's members[0..idx) (partial Fisher-Yates, E:316-325), then ascending order.
+template <typename T, int G>
+__device__ int select_finish(const DynParams& p, Ctx<T, G>& c, int n_p, int* out, int count, int idx,
+                             bool want_fill) {
+  if (count < n_p && want_fill) {
     int need = n_p - count;
     if (need > idx) need = idx;
-    if (lane == 0) {
+    if (c.lane == 0) {
       long long st = c.rng;
       for (int t = 0; t < need; ++t) {
         int r = t + (int)(rand_next(&st) % (long long)(idx - t));
@@ -767,19 +795,180 @@ __device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl,
     count += need;
   }
   c.w.sync();
-  if (p.dump_buf && c.cur_f == 0 && lane == 0 && c.nsel < 8192)
-    p.dump_buf[2 * N + c.nsel] = __longlong_as_double(c.rng);
+  if (p.dump_buf && c.cur_f == 0 && c.lane == 0 && c.nsel < 8192)
+    p.dump_buf[2 * p.g.N + c.nsel] = __longlong_as_double(c.rng);
   ++c.nsel;
-  // ascending sort of out[0..count) (distinct VN ids): rank sort through members[]
-  for (int i = lane; i < count; i += G) {
+  for (int i = c.lane; i < count; i += G) {
     int v = out[i], r = 0;
     for (int q = 0; q < count; ++q) r += out[q] < v;
     c.members[r] = v;
   }
   c.w.sync();
-  for (int i = lane; i < count; i += G) out[i] = c.members[i];
+  for (int i = c.lane; i < count; i += G) out[i] = c.members[i];
   c.w.sync();
   return count;
+}
+
+template <typename T, int G>
+__device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl, int n_p, int* out) {
+  if (p.fast_sel && !excl) {  // maintained histogram + group bitmaps
+    const int N = p.g.N, n_g = p.n_g, lane = c.lane, W = (N + 31) >> 5;
+    int sel_total;
+    const int k_star = kstar_of(c, c.hist, n_g, n_p, &sel_total);
+    const int thr = n_g - k_star, fill = thr - 1;
+    const bool mat = k_star < n_g && sel_total < n_p;  // fill members needed
+    const int fill_size = mat ? c.hist[fill] : 0;
+    const int need = mat ? min(n_p - sel_total, fill_size) : 0;
+    // few picks from a big group: Fisher-Yates on the implicit member list
+    // (rank queries on the group bitmap) instead of materialising it
+    const bool lazy = mat && 4 * need <= fill_size;
+    const unsigned* bits = c.gbits;
+    int* wpre = c.members;  // lazy: members before each bitmap word
+    int count = 0, idx = 0;
+    if (sel_total > 0 || mat) {
+      for (int base = 0; base < W; base += G) {
+        const int wi = base + lane;
+        unsigned sw = 0u, fw = 0u;
+        if (wi < W) {
+          if (sel_total > 0)
+            for (int q = thr; q < n_g; ++q)
+              if (c.hist[q]) sw |= bits[q * W + wi];
+          if (mat) fw = bits[fill * W + wi];
+        }
+        const int packed = __popc(sw) | (__popc(fw) << 16);
+        const int incl = c.w.incl_scan(packed);
+        const int tot = c.w.shfl(incl, G - 1);
+        int ps = count + ((incl - packed) & 0xffff);
+        int pf = idx + ((incl - packed) >> 16);
+        while (sw) {
+          out[ps++] = wi * 32 + __ffs(sw) - 1;
+          sw &= sw - 1;
+        }
+        if (lazy) {
+          if (wi < W) wpre[wi] = pf;
+        } else {
+          while (fw) {
+            c.members[pf++] = wi * 32 + __ffs(fw) - 1;
+            fw &= fw - 1;
+          }
+        }
+        count += tot & 0xffff;
+        idx += tot >> 16;
+      }
+    }
+    c.w.sync();
+    if (!lazy) return select_finish(p, c, n_p, out, count, idx, mat);
+    // lazy partial Fisher-Yates (E:316-325), warp-uniform; overrides (pos, value)
+    int* ov = c.members + W;
+    const unsigned* fb = bits + (long long)fill * W;
+    auto member_at = [&](int pos, int n_ov) -> int {
+      int hit = -1;  // latest override of pos
+      for (int i0 = 0; i0 < n_ov; i0 += G) {
+        const bool h = i0 + lane < n_ov && ov[2 * (i0 + lane)] == pos;
+        const unsigned bal = c.w.ballot(h);
+        if (bal) hit = c.w.shfl(h ? ov[2 * (i0 + lane) + 1] : 0, 31 - __clz(bal));
+      }
+      if (hit >= 0) return hit;
+      int nle = 0;
+      for (int base = 0; base < W; base += G) {
+        const unsigned bal = c.w.ballot(base + lane < W && wpre[base + lane] <= pos);
+        nle += __popc(bal);
+        if (bal != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
+      }
+      const int wsel = nle - 1;
+      return wsel * 32 + (int)__fns(fb[wsel], 0, pos - wpre[wsel] + 1);
+    };
+    long long st = c.rng;
+    for (int t = 0; t < need; ++t) {
+      const int r = t + (int)(rand_next(&st) % (long long)(idx - t));
+      const int vr = member_at(r, t);
+      if (t + 1 < need) {
+        const int vt = member_at(t, t);
+        c.w.sync();
+        if (lane == 0) {
+          ov[2 * t] = r;
+          ov[2 * t + 1] = vt;
+        }
+      }
+      if (lane == 0) out[count + t] = vr;
+      c.w.sync();
+    }
+    c.rng = st;
+    return select_finish(p, c, n_p, out, count + need, idx, false);
+  }
+  if (p.fast_sel) {  // excluded set (ME-LMD-CIRBP top-up): maintained group bytes
+    const int N = p.g.N, n_g = p.n_g, lane = c.lane;
+    for (int q = lane; q < n_g; q += G) c.sizes[q] = c.hist[q];
+    c.w.sync();
+    for (int n0 = 4 * lane; n0 < N; n0 += 4 * G) {  // histogram of the non-excluded VNs
+      const unsigned xv = *(const unsigned*)(excl + n0);
+      if (!xv) continue;
+      const unsigned wv = *(const unsigned*)(c.gid + n0);
+      for (int b = 0; b < 4 && n0 + b < N; ++b)
+        if ((xv >> (8 * b)) & 0xff) atomicSub(&c.sizes[(wv >> (8 * b)) & 0xff], 1);
+    }
+    c.w.sync();
+    int sel_total;
+    const int k_star = kstar_of(c, c.sizes, n_g, n_p, &sel_total);
+    const int thr = n_g - k_star;
+    const int fill = n_g - k_star - 1;
+    const bool want_fill = k_star < n_g && sel_total < n_p;
+    int count = 0, idx = 0;
+    for (int base = 0; base < N; base += 4 * G) {  // 4 VNs per lane, ascending
+      const int n0 = base + 4 * lane;
+      const unsigned wv = n0 < N ? *(const unsigned*)(c.gid + n0) : 0u;
+      const unsigned xv = n0 < N ? *(const unsigned*)(excl + n0) : 0u;
+      int sel = 0, fil = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int gb = (wv >> (8 * b)) & 0xff;
+        const bool in = n0 + b < N && !((xv >> (8 * b)) & 0xff);
+        sel += in && gb >= thr;
+        fil += in && want_fill && gb == fill;
+      }
+      const int packed = sel | (fil << 8);
+      const int incl = c.w.incl_scan(packed);
+      const int tot = c.w.shfl(incl, G - 1);
+      int ps = count + ((incl - packed) & 0xff);
+      int pf = idx + ((incl - packed) >> 8);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int gb = (wv >> (8 * b)) & 0xff;
+        if (n0 + b >= N) break;
+        if ((xv >> (8 * b)) & 0xff) continue;
+        if (gb >= thr) out[ps++] = n0 + b;
+        else if (want_fill && gb == fill) c.members[pf++] = n0 + b;
+      }
+      count += tot & 0xff;
+      idx += tot >> 8;
+    }
+    c.w.sync();
+    return select_finish(p, c, n_p, out, count, idx, want_fill);
+  }
+  const int N = p.g.N, n_g = p.n_g, lane = c.lane;
+  for (int q = lane; q < n_g; q += G) c.sizes[q] = 0;
+  c.w.sync();
+  for (int n = lane; n < N; n += G)
+    if (!excl || !excl[n]) atomicAdd(&c.sizes[ci_group(c.ci[n], n_g)], 1);
+  c.w.sync();
+  int sel_total;
+  const int k_star = kstar_of(c, c.sizes, n_g, n_p, &sel_total);
+  const int thr = n_g - k_star, fill = thr - 1;
+  const bool want_fill = k_star < n_g && sel_total < n_p;
+  int count = 0, idx = 0;
+  for (int base = 0; base < N; base += G) {
+    const int n = base + lane;
+    int gi = -1;
+    if (n < N && (!excl || !excl[n])) gi = ci_group(c.ci[n], n_g);
+    const bool s = gi >= thr, f = want_fill && gi == fill;
+    const unsigned bs = c.w.ballot(s), bf = c.w.ballot(f);
+    if (s) out[count + __popc(bs & c.w.lt)] = n;
+    if (f) c.members[idx + __popc(bf & c.w.lt)] = n;
+    count += __popc(bs);
+    idx += __popc(bf);
+  }
+  c.w.sync();
+  return select_finish(p, c, n_p, out, count, idx, want_fill);
 }
 
 // sort ints ascending in place (distinct values), via members[] scratch
@@ -901,6 +1090,18 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // 
       c.p0t[n] = pt;
       c.ci[n] = Num<T>::abs_(pt - p0(acc));
     }
+  if (p.fast_sel) {
+    const int W = (g.N + 31) >> 5;
+    for (int q = lane; q < p.n_g; q += G) c.hist[q] = 0;
+    for (int q = lane; q < p.n_g * W; q += G) c.gbits[q] = 0u;
+    c.w.sync();
+    for (int n = lane; n < g.N; n += G) {
+      const int gi = ci_group(c.ci[n], p.n_g);
+      c.gid[n] = (uint8_t)gi;
+      atomicAdd(&c.hist[gi], 1);
+      atomicOr(&c.gbits[gi * W + (n >> 5)], 1u << (n & 31));
+    }
+  }
   if (p.kind == KIND_ME_LMD_CIRBP)
     for (int n = lane; n < g.N; n += G) c.inpp[n] = 0;
   c.w.sync();
@@ -1027,7 +1228,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int pv = c.sel[idx];
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
-          propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T, G>(p, c, f, &boundary, &conv);
@@ -1043,7 +1244,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
           if (lane == 0) c.chosen[idx] = e;
-          propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T, G>(p, c, f, &boundary, &conv);
@@ -1176,6 +1377,9 @@ __global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(co
   c.dl0 = (int*)(scr + p.so_dl0);
   c.dl1 = (int*)(scr + p.so_dl1);
   c.sizes = (int*)(scr + p.so_sizes);
+  c.hist = (int*)(scr + p.so_hist);
+  c.gid = (uint8_t*)(bN + p.o_gid);
+  c.gbits = (unsigned*)(bN + p.o_gbits);
   for (;;) {
     unsigned long long f = 0;
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);

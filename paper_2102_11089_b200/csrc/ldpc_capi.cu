@@ -117,7 +117,10 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.o_pretot = take(ci ? N * sizeof(T) : 0);
   p.o_ci = take(ci ? N * sizeof(T) : 0);
   p.o_p0t = take(ci ? N * sizeof(T) : 0);
-  p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? N : 0);
+  p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? (N + 3) / 4 * 4 : 0);
+  p.fast_sel = (me && s->kind != KIND_ME_RBP && s->n_g <= 255) ? 1 : 0;
+  p.o_gid = take(p.fast_sel ? (N + 3) / 4 * 4 : 0);
+  p.o_gbits = take(p.fast_sel ? (long long)s->n_g * ((N + 31) / 32) * 4 : 0);
   p.o_members = take(me ? std::max(N, np) * 4 : 0);
   p.o_sel = take(me ? np * 4 : 0);
   p.o_chosen = take(s->kind == KIND_ME_LMD_CIRBP ? np * 4 : 0);
@@ -149,6 +152,7 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.so_dl0 = (int)stake(dl * 4);
   p.so_dl1 = (int)stake(dl * 4);
   p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
+  p.so_hist = (int)stake(p.fast_sel ? s->n_g * 4 : 0);
   p.scratch_bytes = (int)align16(so);
 }
 

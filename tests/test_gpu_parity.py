@@ -115,7 +115,18 @@ def test_minsum_and_new_schedules(kind):
     _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 5, "kernel": "minsum", "n_p": 4}))
 
 
-@pytest.mark.parametrize("kind", ["rbp", "cirbp", "lmd_cirbp", "flooding"])
+@pytest.mark.parametrize("kind,n_g,n_p", [("me_cirbp", 1, 1), ("me_cirbp", 48, 1), ("me_cirbp", 300, 4),
+                                           ("me_cirbp", 16, 64), ("me_lmd_cirbp", 48, 4),
+                                           ("me_lmd_cirbp", 300, 4), ("me_lmd_cirbp", 16, 64)])
+def test_me_selection_variants(kind, n_g, n_p):
+    """Alg.-4 selection: maintained group bitmaps (n_g <= 32 warp k*, n_g > 32
+    serial k*), the excluded-set path (ME-LMD top-up) and the n_g > 255 rescan."""
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 1.5, seed=11, start=0, count=400)
+    _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 4, "n_p": n_p, "n_g": n_g}))
+
+
+@pytest.mark.parametrize("kind", ["rbp", "cirbp", "lmd_cirbp", "flooding", "me_cirbp", "me_lmd_cirbp"])
 def test_state_placements_match(kind):
     """Shared-memory, split and HBM-resident frame state give identical answers."""
     spec, g = load_code("C0")

@@ -20,15 +20,19 @@ flags = sys.argv[4:]
 placement = next((f for f in flags if f in ("smem", "split", "hbm", "trees")), "hbm" if "global" in flags else "auto")
 prec = "f32" if "f32" in flags else "f64"
 n_p = 4
+imax_over = None
 for f in flags:
     if f.startswith("n_p="):
         n_p = int(f[4:])
-spec = getattr(configs, f"make_{key.lower()}_code")()
+    if f.startswith("imax="):
+        imax_over = int(f[5:])
+spec = getattr(configs, f"make_{('c2' if key == 'C4' else key).lower()}_code")()
 imax = {"C0": 5, "C1": 3, "C2": 3, "C3": 10, "C4": 20}[key]
 eb = {"C0": 2.0, "C1": 2.0, "C2": 1.0, "C3": 1.0, "C4": 0.0}[key]
 if key == "C4":
     spec = configs.make_c2_code()
 llr = torch.from_numpy(llr_batch(spec, eb, 0, 0, nfr)).cuda()
+imax = imax_over or imax
 cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=n_p, precision=prec)
 decode_batch(spec, llr[:1], cfg, placement=placement)
 torch.cuda.synchronize()
