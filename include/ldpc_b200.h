@@ -74,6 +74,8 @@ typedef struct {
   int32_t max_resident;   /* 0 = auto; else cap on concurrently decoded frames */
   int32_t placement;      /* dynamic schedules: 0 auto, 1 all state in HBM, 2 per-edge state in HBM,
                              3 all in shared memory, 4 per-edge + per-VN state in HBM (trees in smem) */
+  int32_t want_trace;     /* 1: keep pre_total for every kind and allow ldpc_decode_traced outputs
+                             (decode(..., want_trace=True), schedules.py:111-158) */
 } ldpc_sched_t;
 
 /* Build the device-resident Tanner graph (edge ids in (check, vn) order,
@@ -100,6 +102,22 @@ int ldpc_decode(const ldpc_graph_t* g, const void* llr, int64_t B, const ldpc_sc
                 int8_t* u_hat, int64_t* props, uint8_t* converged, int64_t* counters,
                 int32_t* biterr, int32_t* biterr_info, int32_t* kappa_hits, int32_t* kappa_trials,
                 void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/* ldpc_decode plus the reference's want_trace outputs (s->want_trace must be 1):
+ *   trace[B][i_max+1][2N] float64 (may be NULL): per iteration boundary k the
+ *   totals, then the pre-totals (E:192-217; flooding/layered: the next
+ *   flooding pass's totals, E:768-782), rows after convergence repeated
+ *   (E:211-217) -- DecodeResult.trace_llrs (schedules.py:57);
+ *   j_counts[i_max+1][n_gamma][2] uint64 (may be NULL), ACCUMULATED (the
+ *   caller zeroes it): VNs with D = |p0(total) - p0(pre_total)| >= gammas[gi]
+ *   that are correct (total >= 0) / wrong, per boundary -- the counts
+ *   sim._sim_block forms from the trace for mc_j_gamma (sim.py:172-183,
+ *   339-353), fused so the trace need not be stored.  gammas: device float64. */
+int ldpc_decode_traced(const ldpc_graph_t* g, const void* llr, int64_t B, const ldpc_sched_t* s,
+                       int8_t* u_hat, int64_t* props, uint8_t* converged, int64_t* counters,
+                       int32_t* biterr, int32_t* biterr_info, int32_t* kappa_hits, int32_t* kappa_trials,
+                       double* trace, const double* gammas, int32_t n_gamma, uint64_t* j_counts,
+                       void* workspace, size_t ws_bytes, void* cuda_stream);
 
 /* Algorithm-4 VN selection (schedules.py:60-79, E:292-352) on the device:
  * ci[N] float64, mask[N] uint8 (NULL = all), out[n_p] int32; *count_dev gets

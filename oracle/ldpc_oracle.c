@@ -20,6 +20,9 @@
  *   KIND_LAYERED : row-layered BP, checks m = 0..M-1 in order; for each check
  *                  v2c = clamp(total - c2v) over N(m), c2v' = cn_msg(v2c),
  *                  total += c2v' - c2v (the E:147 incremental form).
+ *                  Trace rows (want_trace): pre_total = chl + sum of the
+ *                  C2V messages a flooding pass would send from the current
+ *                  extrinsics v2c = clamp(total - c2v) (E:768-782 semantics).
  *   KIND_ME_RBP  : multi-edge RBP; per round the n_p largest residuals
  *                  (ties -> lowest edge id) are propagated in ascending edge
  *                  id, each committing its then-current pre_c2v.  Boundaries
@@ -843,12 +846,20 @@ static int64_t decode_flooding(const graph_t* g, const real* chl, const sched_t*
   return c->i_max > 0 ? it * E : 0;
 }
 
+/* Layered trace pre-totals (see header): flooding pass from v2c = clamp(total - c2v).
+ * v2c / pre are scratch here (every layer recomputes them before use). */
+static void layered_pre_totals(const graph_t* g, const real* chl, int kernel, state_t* s) {
+  for (int64_t e = 0; e < g->n_edges; ++e) s->v2c[e] = clampv(s->total[g->edge_vn[e]] - s->c2v[e]);
+  flood_pre_totals(g, chl, kernel, s);
+}
+
 /* Layered (new, see header). */
 static int64_t decode_layered(const graph_t* g, const real* chl, const sched_t* c, state_t* s,
                               int* conv) {
   int64_t E = g->n_edges, N = g->n_vars;
   for (int64_t e = 0; e < E; ++e) s->c2v[e] = 0.0;
   for (int64_t n = 0; n < N; ++n) s->total[n] = chl[n];
+  if (s->trace) layered_pre_totals(g, chl, c->kernel, s);
   record_boundary(0, g, c->k_info, s);
   *conv = 0;
   int64_t it = 0;
@@ -864,6 +875,7 @@ static int64_t decode_layered(const graph_t* g, const real* chl, const sched_t* 
       s->counters[C_PROP] += b - a;
       s->counters[C_V2C] += b - a;
     }
+    if (s->trace) layered_pre_totals(g, chl, c->kernel, s);
     record_boundary(it, g, c->k_info, s);
     if (syndrome_ok(s->total, g)) {
       *conv = 1;

@@ -22,12 +22,13 @@ class LdpcSched(C.Structure):
                 ("n_p", C.c_int32), ("n_g", C.c_int32), ("k_info", C.c_int32),
                 ("gamma", C.c_double), ("selection_seed", C.c_int64),
                 ("precision", C.c_int32), ("llr_f64", C.c_int32),
-                ("max_resident", C.c_int32), ("placement", C.c_int32)]
+                ("max_resident", C.c_int32), ("placement", C.c_int32),
+                ("want_trace", C.c_int32)]
 
 
 # every exported symbol of include/ldpc_b200.h
 EXPORTS = ("ldpc_graph_create", "ldpc_graph_destroy", "ldpc_graph_info", "ldpc_workspace_size",
-           "ldpc_decode", "ldpc_select_vns", "ldpc_set_step_log", "ldpc_set_state_dump",
+           "ldpc_decode", "ldpc_decode_traced", "ldpc_select_vns", "ldpc_set_step_log", "ldpc_set_state_dump",
            "ldpc_generate_awgn",
            "ldpc_last_launch_count",
            "ldpc_strerror", "ldpc_version")
@@ -54,6 +55,7 @@ def lib():
     L.ldpc_graph_info.argtypes = [P, P]
     L.ldpc_workspace_size.argtypes = [P, C.POINTER(LdpcSched), I64, C.POINTER(SZ)]
     L.ldpc_decode.argtypes = [P, P, I64, C.POINTER(LdpcSched)] + [P] * 8 + [P, SZ, P]
+    L.ldpc_decode_traced.argtypes = [P, P, I64, C.POINTER(LdpcSched)] + [P] * 8 + [P, P, I32, P] + [P, SZ, P]
     L.ldpc_select_vns.argtypes = [P, P, I32, I32, I32, I64, P, P, P]
     L.ldpc_set_step_log.argtypes = [P, I32]
     L.ldpc_generate_awgn.argtypes = [I32, I32, I64, C.c_double, C.c_uint64, I64, P, I32, P]

@@ -76,6 +76,10 @@ struct DynParams {
   int scratch_bytes;      // per-warp shared scratch
   int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes, so_hist;
   int fast_sel;           // ME kinds with n_g <= 255: maintained groups + histogram
+  // want_trace (E:192-217): pre_total upkeep for every kind, per-boundary rows
+  // and fused J(gamma) counts (sim.py:172-183)
+  int pt_on;              // maintain pre_total (always for CI kinds)
+  TraceOut tr;
 };
 
 template <typename T, int G>
@@ -487,7 +491,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     c.stage[r.w + (r.x - r.y)] = c.in[r.x];
   }
   w.sync();
-  const bool dup = CI && g.hop_dup[e_star] != 0;
+  const bool PT = CI || p.pt_on;  // pre_total upkeep (E:171)
+  const bool dup = PT && g.hop_dup[e_star] != 0;
   // two-hop refresh (E:161-176), G edges per pass in reference order
   for (int base = 0; base < n_items; base += G) {
     const int t = base + lane;
@@ -500,7 +505,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       // independent loads first (the pre[] store below would otherwise pin them)
       const T cg = c.c2v[ge];
       T opre = T(0);
-      if (CI) {
+      if (PT) {
         j = g.edge_vn[ge];
         opre = c.pre[ge];
       }
@@ -521,20 +526,22 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         }
         np_ = r.z > 1 ? clampv(sign * mag) : T(0);
       }
-      if (CI) delta = np_ - opre;
+      if (PT) delta = np_ - opre;
       c.pre[ge] = np_;
       T rv = Num<T>::abs_(np_ - cg);
       if (STORED) c.res[ge] = rv;
       if (RT) c.nk[t] = Num<T>::key(rv);
     }
-    if (CI) {
+    if (PT) {
       if (!dup) {
         if (valid) {
           T pt = c.pretot[j] + delta;  // E:171
           c.pretot[j] = pt;
-          const T cv = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
-          c.ci[j] = cv;
-          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+          if (CI) {
+            const T cv = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
+            c.ci[j] = cv;
+            if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+          }
         }
       } else {
         // the same VN reached through two checks (4-cycle): keep the reference's order
@@ -546,7 +553,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           w.sync();
         }
         const bool last = valid && ((peers >> lane) >> 1) == 0;
-        if (last) {
+        if (CI && last) {
           const T cv = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
           c.ci[j] = cv;
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
@@ -695,6 +702,12 @@ __device__ __forceinline__ void fill_remaining(const DynParams& p, long long f, 
   w.sync();
 }
 
+template <typename T, int G>
+__device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, const T* pretot, long long f, int k,
+                                           bool conv, const Grp<G>& w) {
+  trace_boundary_rows<T, G>(p.tr, p.g.N, p.i_max, total, pretot, f, k, conv, w);
+}
+
 // single-edge boundary rule (E:377-384): returns true when decoding stops
 template <typename T, int G>
 __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c, long long f, bool* conv) {
@@ -705,8 +718,10 @@ __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c
   if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
     *conv = true;
     fill_remaining<G>(p, f, k, c.w);
+    trace_rows<T, G>(p, c.total, c.pretot, f, k, true, c.w);
     return true;
   }
+  trace_rows<T, G>(p, c.total, c.pretot, f, k, false, c.w);
   return false;
 }
 
@@ -720,6 +735,7 @@ __device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int
       *conv = true;
       fill_remaining<G>(p, f, *boundary, c.w);
     }
+    trace_rows<T, G>(p, c.total, c.pretot, f, *boundary, *conv, c.w);
     ++(*boundary);
     if (*conv) break;
   }
@@ -1081,14 +1097,16 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // 
     for (int e = a; e < b; ++e) c.pre[e] = cn_msg_cached<T, KERNEL>(c.in, a, b, e);
   }
   c.w.sync();
-  if (CI)
+  if (CI || p.pt_on)
     for (int n = lane; n < g.N; n += G) {
       T acc = chl(n);
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
-      c.pretot[n] = acc;
-      const T pt = p0(c.total[n]);
-      c.p0t[n] = pt;
-      c.ci[n] = Num<T>::abs_(pt - p0(acc));
+      c.pretot[n] = acc;  // E:121-125
+      if (CI) {
+        const T pt = p0(c.total[n]);
+        c.p0t[n] = pt;
+        c.ci[n] = Num<T>::abs_(pt - p0(acc));
+      }
     }
   if (p.fast_sel) {
     const int W = (g.N + 31) >> 5;
@@ -1132,6 +1150,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   if (ci_kind) init_state<T, KERNEL, true, G>(p, c, f);
   else init_state<T, KERNEL, false, G>(p, c, f);
   record_boundary<T, G>(p, c.total, f, 0, c.w);
+  trace_rows<T, G>(p, c.total, c.pretot, f, 0, false, c.w);
   auto rleaf = [&](int e) -> Key { return res_key<T, false, G>(c, e); };
   auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
 

@@ -27,3 +27,26 @@ inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16) {
   }
 }
 void* ldpc_fixed_kernel(int f64, int kernel, int layered);
+
+namespace ldpc {
+// traced flooding / layered decode (fixed_trace.cu): one warp per frame
+constexpr int kTraceWarps = 8;
+struct FixedTraceParams {
+  DevGraph g;
+  int i_max, k_info;
+  const void* llr;
+  int llr_f64;
+  long long B;
+  int8_t* u_hat;
+  long long* prop;
+  uint8_t* conv;
+  long long* counters;
+  int* biterr;
+  int* biterr_info;
+  unsigned long long* next;
+  unsigned char* ws;
+  long long slot_bytes;
+  TraceOut tr;
+};
+}  // namespace ldpc
+void* ldpc_fixed_trace_kernel(int f64, int kernel, int layered);

@@ -114,7 +114,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   // N part
   o = 0;
   p.o_total = take(N * sizeof(T));
-  p.o_pretot = take(ci ? N * sizeof(T) : 0);
+  p.o_pretot = take(ci || s->want_trace ? N * sizeof(T) : 0);
+  p.pt_on = s->want_trace && !ci ? 1 : 0;
   p.o_ci = take(ci ? N * sizeof(T) : 0);
   p.o_p0t = take(ci ? N * sizeof(T) : 0);
   p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? (N + 3) / 4 * 4 : 0);
@@ -248,6 +249,28 @@ struct FixedPlan {
   long long ws_bytes;
 };
 
+// traced flooding / layered (fixed_trace.cu): one warp per frame, state in HBM
+struct FixedTracePlan {
+  FixedTraceParams p;
+  int blocks;
+  long long ws_bytes;
+};
+
+template <typename T>
+int fixed_trace_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedTracePlan& pl) {
+  memset(&pl, 0, sizeof(pl));
+  pl.p.slot_bytes = align16((3ll * G->d.E + 3ll * G->d.N) * sizeof(T));
+  void* fn = ldpc_fixed_trace_kernel(sizeof(T) == 8, s->kernel, s->kind == KIND_LAYERED);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTraceWarps * 32, 0) != cudaSuccess || occ < 1) occ = 1;
+  long long blocks = std::min<long long>((long long)occ * sm_count(), (B + kTraceWarps - 1) / kTraceWarps);
+  if (s->max_resident > 0) blocks = std::min<long long>(blocks, std::max(1, s->max_resident / kTraceWarps));
+  const long long cap = std::max<long long>(1, (24ll << 30) / (pl.p.slot_bytes * kTraceWarps));
+  pl.blocks = (int)std::max<long long>(1, std::min(blocks, cap));
+  pl.ws_bytes = 256 + (long long)pl.blocks * kTraceWarps * pl.p.slot_bytes;
+  return LDPC_OK;
+}
+
 template <typename T>
 int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPlan& pl) {
   memset(&pl, 0, sizeof(pl));
@@ -292,6 +315,7 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if (!is_dynamic(s->kind) && G->max_dc > kTileEdges) return LDPC_ERR_UNSUPPORTED;
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
   if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
+  if (s->want_trace != 0 && s->want_trace != 1) return LDPC_ERR_INVALID;
   return LDPC_OK;
 }
 
@@ -299,10 +323,37 @@ template <typename T>
 int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sched_t* s,
                 int8_t* u_hat, int64_t* props, uint8_t* conv, int64_t* counters, int32_t* biterr,
                 int32_t* biterr_info, int32_t* kh, int32_t* kt, void* ws, size_t ws_bytes,
-                cudaStream_t st) {
+                const TraceOut& tr, cudaStream_t st) {
   g_last_launches = 0;
   if (B == 0) return LDPC_OK;
   unsigned long long* next = (unsigned long long*)ws;
+  if (!is_dynamic(s->kind) && s->want_trace) {
+    FixedTracePlan pl;
+    if (int rc = fixed_trace_plan<T>(G, s, B, pl)) return rc;
+    if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
+    FixedTraceParams& p = pl.p;
+    p.g = G->d;
+    p.i_max = s->i_max;
+    p.k_info = s->k_info;
+    p.llr = llr;
+    p.llr_f64 = s->llr_f64;
+    p.B = B;
+    p.u_hat = u_hat;
+    p.prop = (long long*)props;
+    p.conv = conv;
+    p.counters = (long long*)counters;
+    p.biterr = biterr;
+    p.biterr_info = biterr_info;
+    p.next = next;
+    p.ws = (unsigned char*)ws + 256;
+    p.tr = tr;
+    if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
+    void* fn = ldpc_fixed_trace_kernel(sizeof(T) == 8, s->kernel, s->kind == KIND_LAYERED);
+    void* args[] = {&p};
+    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(kTraceWarps * 32), args, 0, st))) return rc;
+    g_last_launches = 1;
+    return LDPC_OK;
+  }
   if (is_dynamic(s->kind)) {
     DynPlan pl;
     if (int rc = dyn_plan<T>(G, s, B, pl)) return rc;
@@ -336,6 +387,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.dump_buf = g_dump_buf;
     p.log_cap = g_log_cap;
     p.ws = (unsigned char*)ws + 256;
+    p.tr = tr;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
     void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16);
     void* args[] = {&p};
@@ -768,6 +820,11 @@ int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B,
       int rc = s->precision == LDPC_F64 ? dyn_plan<double>(G, s, B, pl) : dyn_plan<float>(G, s, B, pl);
       if (rc) return rc;
       ws = pl.ws_bytes;
+    } else if (s->want_trace) {
+      FixedTracePlan pl;
+      int rc = s->precision == LDPC_F64 ? fixed_trace_plan<double>(G, s, B, pl) : fixed_trace_plan<float>(G, s, B, pl);
+      if (rc) return rc;
+      ws = pl.ws_bytes;
     } else {
       FixedPlan pl;
       int rc = s->precision == LDPC_F64 ? fixed_plan<double>(G, s, B, pl) : fixed_plan<float>(G, s, B, pl);
@@ -787,11 +844,31 @@ int ldpc_decode(const ldpc_graph_t* G, const void* llr, int64_t B, const ldpc_sc
   if (B > 0 && (!llr || !u_hat || !props || !converged || !counters || !biterr || !biterr_info || !workspace))
     return LDPC_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
+  const TraceOut tr{nullptr, nullptr, 0, nullptr};
   if (s->precision == LDPC_F64)
     return decode_impl<double>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
-                               kappa_hits, kappa_trials, workspace, ws_bytes, st);
+                               kappa_hits, kappa_trials, workspace, ws_bytes, tr, st);
   return decode_impl<float>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
-                            kappa_hits, kappa_trials, workspace, ws_bytes, st);
+                            kappa_hits, kappa_trials, workspace, ws_bytes, tr, st);
+}
+
+int ldpc_decode_traced(const ldpc_graph_t* G, const void* llr, int64_t B, const ldpc_sched_t* s,
+                       int8_t* u_hat, int64_t* props, uint8_t* converged, int64_t* counters,
+                       int32_t* biterr, int32_t* biterr_info, int32_t* kappa_hits, int32_t* kappa_trials,
+                       double* trace, const double* gammas, int32_t n_gamma, uint64_t* j_counts,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  if (int rc = validate(G, s, B)) return rc;
+  if (!s->want_trace) return LDPC_ERR_INVALID;
+  if (B > 0 && (!llr || !u_hat || !props || !converged || !counters || !biterr || !biterr_info || !workspace))
+    return LDPC_ERR_INVALID;
+  if (j_counts && (n_gamma < 1 || !gammas)) return LDPC_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const TraceOut tr{trace, gammas, j_counts ? n_gamma : 0, (unsigned long long*)j_counts};
+  if (s->precision == LDPC_F64)
+    return decode_impl<double>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
+                               kappa_hits, kappa_trials, workspace, ws_bytes, tr, st);
+  return decode_impl<float>(G, llr, B, s, u_hat, props, converged, counters, biterr, biterr_info,
+                            kappa_hits, kappa_trials, workspace, ws_bytes, tr, st);
 }
 
 int ldpc_select_vns(const double* ci, const uint8_t* mask, int32_t N, int32_t n_g, int32_t n_p,

@@ -157,7 +157,14 @@ __device__ __forceinline__ T cn_msg_cached(const T* in, int a, int b, int skip) 
   }
 }
 
-// ------------------------------------------------------------ warp helpers
+// want_trace outputs (E:192-217, schedules.py:57) and fused J(gamma) counts
+// (sim.py:172-183).
+struct TraceOut {
+  double* trace;           // [B][i_max+1][2N]: totals then pre-totals, or null
+  const double* gammas;    // [n_gamma] (device)
+  int n_gamma;
+  unsigned long long* jc;  // [i_max+1][n_gamma][2]: (correct, wrong) VNs with D >= gamma, or null
+};
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -300,5 +307,44 @@ struct Grp {
     return m;
   }
 };
+
+// Rows of boundary k (E:204-207) -- and, once converged, of every later
+// boundary (E:215-217) -- plus their J(gamma) counts, D = |p0(total) -
+// p0(pre_total)| in float64 like the reference's post-processing of the trace.
+template <typename T, int G>
+__device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* total, const T* pretot, long long f,
+                                    int k, bool conv, const Grp<G>& w) {
+  if (!to.trace && !to.jc) return;
+  const int last = conv ? I : k;
+  if (to.trace)
+    for (int kk = k; kk <= last; ++kk) {
+      double* row = to.trace + (f * (I + 1) + kk) * 2ll * N;
+      for (int n = w.lane; n < N; n += G) {
+        row[n] = (double)total[n];
+        row[N + n] = (double)pretot[n];
+      }
+    }
+  if (to.jc)
+    for (int gi = 0; gi < to.n_gamma; ++gi) {
+      const double gm = to.gammas[gi];
+      int ok = 0, bad = 0;
+      for (int n = w.lane; n < N; n += G) {
+        const double t = (double)total[n];
+        const double d = fabs(p0(t) - p0((double)pretot[n]));
+        if (d >= gm) {
+          if (t >= 0.0) ++ok;
+          else ++bad;
+        }
+      }
+      ok = w.rsum(ok);
+      bad = w.rsum(bad);
+      if (w.lane == 0)
+        for (int kk = k; kk <= last; ++kk) {
+          if (ok) atomicAdd(&to.jc[((long long)kk * to.n_gamma + gi) * 2], (unsigned long long)ok);
+          if (bad) atomicAdd(&to.jc[((long long)kk * to.n_gamma + gi) * 2 + 1], (unsigned long long)bad);
+        }
+    }
+  w.sync();
+}
 
 }  // namespace ldpc

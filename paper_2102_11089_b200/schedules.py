@@ -139,14 +139,15 @@ _code_cache = {}
 PLACEMENTS = {"auto": 0, "hbm": 1, "split": 2, "smem": 3, "trees": 4}
 
 
-def _sched(config: ScheduleConfig, k_info: int, llr_f64: bool, max_resident=0, placement="auto"):
+def _sched(config: ScheduleConfig, k_info: int, llr_f64: bool, max_resident=0, placement="auto",
+           want_trace=False):
     seed = int(config.selection_seed) & 0xFFFFFFFFFFFFFFFF
     if seed >= 1 << 63:
         seed -= 1 << 64
     return _native.LdpcSched(KIND_IDS[config.kind], KERNELS[config.kernel], config.i_max,
                              config.n_p, config.n_g, int(k_info), float(config.gamma), seed,
                              PRECISIONS[config.precision], 1 if llr_f64 else 0,
-                             int(max_resident), PLACEMENTS[placement])
+                             int(max_resident), PLACEMENTS[placement], 1 if want_trace else 0)
 
 
 def _ptr(t):
@@ -154,7 +155,8 @@ def _ptr(t):
 
 
 def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, device=None,
-                 stream=None, out=None, max_resident=0, placement="auto", force_global=False):
+                 stream=None, out=None, max_resident=0, placement="auto", force_global=False,
+                 want_trace=False, gammas=None, j_counts=None):
     """Decode a batch of frames on the GPU.
 
     code: CodeSpec (k_info taken from it) or TannerGraph (pass k_info).
@@ -188,7 +190,8 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
     I = config.i_max
     if force_global:
         placement = "hbm"
-    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, placement)
+    tracing = bool(want_trace) or gammas is not None
+    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, placement, tracing)
     if out is None:
         out = {
             "u_hat": torch.empty((B, dg.N), dtype=torch.int8, device=device),
@@ -203,12 +206,33 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
     ws = dg.workspace(sched, B, device)
     st = stream if stream is not None else torch.cuda.current_stream(device)
     L = _native.lib()
-    rc = L.ldpc_decode(dg.handle, _ptr(llrs), B, C.byref(sched), _ptr(out["u_hat"]), _ptr(out["prop"]),
-                       _ptr(out["converged"]), _ptr(out["counters"]), _ptr(out["bit_errors_at"]),
-                       _ptr(out["info_bit_errors_at"]), _ptr(out["kappa_hits_iter"]),
-                       _ptr(out["kappa_trials_iter"]), _ptr(ws), ws.numel(),
-                       C.c_void_p(st.cuda_stream))
-    _native.check(rc, "ldpc_decode")
+    if not tracing:
+        rc = L.ldpc_decode(dg.handle, _ptr(llrs), B, C.byref(sched), _ptr(out["u_hat"]), _ptr(out["prop"]),
+                           _ptr(out["converged"]), _ptr(out["counters"]), _ptr(out["bit_errors_at"]),
+                           _ptr(out["info_bit_errors_at"]), _ptr(out["kappa_hits_iter"]),
+                           _ptr(out["kappa_trials_iter"]), _ptr(ws), ws.numel(),
+                           C.c_void_p(st.cuda_stream))
+        _native.check(rc, "ldpc_decode")
+    else:
+        trace = None
+        if want_trace and want_trace != "counts":
+            trace = torch.empty((B, I + 1, 2 * dg.N), dtype=torch.float64, device=device)
+            out["trace_llrs"] = trace
+        gam = None
+        if gammas is not None:
+            gam = torch.as_tensor(np.asarray(list(gammas), np.float64), device=device)
+            if gam.numel() < 1:
+                raise ValueError("gammas must be non-empty")
+            if j_counts is None:
+                j_counts = torch.zeros((I + 1, gam.numel(), 2), dtype=torch.int64, device=device)
+            out["j_counts"] = j_counts
+        rc = L.ldpc_decode_traced(dg.handle, _ptr(llrs), B, C.byref(sched), _ptr(out["u_hat"]),
+                                  _ptr(out["prop"]), _ptr(out["converged"]), _ptr(out["counters"]),
+                                  _ptr(out["bit_errors_at"]), _ptr(out["info_bit_errors_at"]),
+                                  _ptr(out["kappa_hits_iter"]), _ptr(out["kappa_trials_iter"]),
+                                  _ptr(trace), _ptr(gam), 0 if gam is None else gam.numel(),
+                                  _ptr(j_counts), _ptr(ws), ws.numel(), C.c_void_p(st.cuda_stream))
+        _native.check(rc, "ldpc_decode_traced")
     out["_launches"] = L.ldpc_last_launch_count()
     return out
 
@@ -224,8 +248,6 @@ def results_to_numpy(out, kind, i_max):
 def decode(code: CodeSpec, channel_llrs, config: ScheduleConfig, graph=None,
            want_trace=False) -> DecodeResult:
     """Run one frame through the configured schedule (schedules.py:111-158)."""
-    if want_trace:
-        raise NotImplementedError("want_trace is not implemented on the GPU path yet")
     if graph is None:
         cache = _code_cache.setdefault(id(code), {})
         if "tanner" not in cache:
@@ -235,7 +257,7 @@ def decode(code: CodeSpec, channel_llrs, config: ScheduleConfig, graph=None,
     chl = np.asarray(channel_llrs, dtype=np.float64)
     if chl.ndim != 1 or len(chl) != graph.n_vars:
         raise ValueError("channel LLR length mismatch")
-    out = decode_batch(graph, chl[None, :], config, k_info=code.k_info)
+    out = decode_batch(graph, chl[None, :], config, k_info=code.k_info, want_trace=bool(want_trace))
     r = results_to_numpy(out, config.kind, config.i_max)
     kh = kt = np.zeros(0, np.int64)
     if config.kind == "cirbp":
@@ -248,7 +270,8 @@ def decode(code: CodeSpec, channel_llrs, config: ScheduleConfig, graph=None,
         counters=Counters.from_array(r["counters"][0]),
         bit_errors_at=r["bit_errors_at"][0].astype(np.int64),
         info_bit_errors_at=r["info_bit_errors_at"][0].astype(np.int64),
-        kappa_hits_iter=kh, kappa_trials_iter=kt, trace_llrs=None)
+        kappa_hits_iter=kh, kappa_trials_iter=kt,
+        trace_llrs=r["trace_llrs"][0] if want_trace else None)
 
 
 def select_vns(ci_values, n_g, n_p, seed, search_set=None):

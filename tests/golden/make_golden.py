@@ -115,7 +115,85 @@ def plan():
     return cases
 
 
+def _trace_work(task):
+    code_key, llrs, sched = task
+    rc, rs = _ref()
+    spec = {"C0": configs.make_c0_code}[code_key]()
+    rspec = _ref_spec(spec)
+    graph = rc.build_tanner(rspec.h)
+    cfg = rs.ScheduleConfig(**sched)
+    return [np.asarray(rs.decode(rspec, row.astype(np.float64), cfg, graph=graph,
+                                 want_trace=True).trace_llrs, np.float64) for row in llrs]
+
+
+def make_trace_golden():
+    """trace.npz: want_trace outputs (schedules.py:57, E:192-217, E:768-782) of
+    the reference on C0 -- full arrays for frame 0, sha256 digests of every
+    frame -- and J(gamma) counts of sim.mc_j_gamma (sim.py:339-353)."""
+    import hashlib
+    _ref()
+    from ldpc_ids import sim as rsim, schedules as rs
+    rc, _ = _ref()
+    spec = configs.make_c0_code()
+    rng = np.random.default_rng(11089)
+    llrs = llr_batch(spec, 1.5, seed=0, start=0, count=5, dtype=np.float32)
+    llrs = np.concatenate([llrs, _tie_frames(spec.h.n_cols, rng)[3:]])
+    ref8 = ["flooding", "rbp", "cirbp", "lmdrbp", "slmdrbp", "lmd_cirbp", "me_cirbp", "me_lmd_cirbp"]
+    scheds = [dict(kind=k, i_max=3, n_p=4) for k in ref8] + [dict(kind="rbp", i_max=3, kernel="minsum")]
+    payload = {"llrs": llrs, "digest": edge_digest(spec), "schedules": np.array([repr(x) for x in scheds])}
+    with ProcessPoolExecutor(max_workers=os.cpu_count()) as pool:
+        futs = [pool.submit(_trace_work, ("C0", llrs, sc)) for sc in scheds]
+        for si, f in enumerate(futs):
+            tr = f.result()
+            payload[f"s{si}_trace0"] = tr[0]
+            payload[f"s{si}_sha"] = np.array([hashlib.sha256(np.ascontiguousarray(t).tobytes()).hexdigest()
+                                              for t in tr])
+    rspec = _ref_spec(spec)
+    gam = [0.0, 0.02, 0.1, 0.3, 0.6]
+    jc = []
+    jcases = [dict(kind="cirbp", i_max=3), dict(kind="rbp", i_max=3), dict(kind="flooding", i_max=3),
+              dict(kind="me_cirbp", i_max=3, n_p=4)]
+    for jc_cfg in jcases:
+        r = rsim.mc_j_gamma(rspec, rs.ScheduleConfig(**jc_cfg), 1.0, gam, 96, master_seed=7)
+        jc.append(np.asarray(r["counts"], np.int64))
+    payload["j_gammas"] = np.array(gam)
+    payload["j_cases"] = np.array([repr(x) for x in jcases])
+    payload["j_counts"] = np.stack(jc)
+    payload["j_ebn0"] = np.float64(1.0)
+    payload["j_frames"] = np.int64(96)
+    payload["j_seed"] = np.int64(7)
+    np.savez_compressed(OUT / "trace.npz", **payload)
+
+
+def make_sim_golden():
+    """sim.npz: CSV records of the reference harness (sim.run_fer_sweep,
+    sim.py:303-316) for a small C0 campaign -- block order, min_frame_errors
+    stopping, per-iteration FER/BER, kappa per iteration."""
+    _ref()
+    from ldpc_ids import sim as rsim, schedules as rs
+    spec = configs.make_c0_code()
+    rspec = _ref_spec(spec)
+    scheds = [dict(kind="cirbp", i_max=3), dict(kind="rbp", i_max=2), dict(kind="flooding", i_max=4),
+              dict(kind="me_cirbp", i_max=3, n_p=4), dict(kind="lmdrbp", i_max=3, kernel="minsum")]
+    camp = rsim.Campaign(code=rspec, schedules=[rs.ScheduleConfig(**x) for x in scheds],
+                         snr_grid=[1.0, 2.0], min_frame_errors=12, max_frames=1500, master_seed=3)
+    recs = rsim.run_fer_sweep(camp)
+    csv_text = rsim.records_to_csv(recs)
+    kp = [str(r.kappa_per_iteration) for r in recs]
+    np.savez_compressed(OUT / "sim.npz", csv=np.array(csv_text), schedules=np.array([repr(x) for x in scheds]),
+                        snr=np.array([1.0, 2.0]), min_frame_errors=np.int64(12), max_frames=np.int64(1500),
+                        seed=np.int64(3), kappa_per_iteration=np.array(kp),
+                        frame_errors_at=np.array([str(r.frame_errors_at) for r in recs]),
+                        bit_errors_at=np.array([str(r.bit_errors_at) for r in recs]))
+
+
 def main():
+    if "--only-trace" in sys.argv:
+        make_trace_golden()
+        return
+    if "--only-sim" in sys.argv:
+        make_sim_golden()
+        return
     t0 = time.time()
     _ref()
     rc, _ = _ref()
@@ -167,6 +245,8 @@ def main():
     kat["rand_seq"] = np.array(seq, np.int64)
     kat["p0_ln3"] = rk.posterior_p0(np.log(3.0))
     np.savez_compressed(OUT / "kat.npz", **{k: np.asarray(v) for k, v in kat.items()})
+    make_trace_golden()
+    make_sim_golden()
     print(f"done in {time.time() - t0:.0f}s")
 
 

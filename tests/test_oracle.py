@@ -95,3 +95,37 @@ def test_golden_schedule_lists_parse():
         assert isinstance(sched, dict)
     z = np.load("tests/golden/c0.npz")
     assert all(isinstance(ast.literal_eval(s), dict) for s in z["schedules"])
+
+
+@pytest.mark.parametrize("si,sched", __import__("tests.util", fromlist=["x"]).trace_golden_cases())
+def test_oracle_trace_matches_reference(si, sched):
+    """want_trace rows (totals, pre-totals per boundary; E:192-217, E:768-782)."""
+    import hashlib
+    z = np.load("tests/golden/trace.npz")
+    spec, g = load_code("C0")
+    cfg = dict(kind="flooding", gamma=0.1, n_p=1, n_g=16, i_max=3, kernel="exact", selection_seed=0)
+    cfg.update(sched)
+    for f, row in enumerate(z["llrs"].astype(np.float64)):
+        r = pyoracle.decode(g, row, cfg["kind"], cfg["kernel"], cfg["i_max"], spec.k_info, cfg["gamma"],
+                            cfg["n_p"], cfg["n_g"], cfg["selection_seed"], want_trace=True)
+        tr = np.ascontiguousarray(r["trace_llrs"], np.float64)
+        if f == 0:
+            np.testing.assert_array_equal(tr, z[f"s{si}_trace0"])
+        assert hashlib.sha256(tr.tobytes()).hexdigest() == z[f"s{si}_sha"][f], (sched, f)
+
+
+def test_oracle_j_gamma_counts_match_reference():
+    """mc_j_gamma (sim.py:339-353) counts from oracle traces of the same frames."""
+    from paper_2102_11089_b200.channel import llr_batch
+    from tests.util import j_counts_from_traces
+    z = np.load("tests/golden/trace.npz")
+    spec, g = load_code("C0")
+    gam = list(z["j_gammas"])
+    llrs = llr_batch(spec, float(z["j_ebn0"]), int(z["j_seed"]), 0, int(z["j_frames"]), dtype=np.float64)
+    for ci, case in enumerate(z["j_cases"]):
+        cfg = dict(kind="flooding", gamma=0.1, n_p=1, n_g=16, i_max=3, kernel="exact", selection_seed=0)
+        cfg.update(ast.literal_eval(str(case)))
+        traces = [pyoracle.decode(g, row, cfg["kind"], cfg["kernel"], cfg["i_max"], spec.k_info,
+                                  cfg["gamma"], cfg["n_p"], cfg["n_g"], cfg["selection_seed"],
+                                  want_trace=True)["trace_llrs"] for row in llrs]
+        np.testing.assert_array_equal(j_counts_from_traces(traces, gam), z["j_counts"][ci], err_msg=str(case))

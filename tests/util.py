@@ -34,3 +34,38 @@ def golden_digest_ok(fname, g):
     d = np.array([g.n_vars, g.n_checks, g.n_edges,
                   int(np.sum(g.edge_cn * 1_000_003 + g.edge_vn * 7) % (1 << 61))], np.int64)
     return bool((z["digest"] == d).all())
+
+
+def p0_vec(llrs):
+    """Stable logistic P(bit = 0) (kernels.posterior_p0 / sim._p0_vec, sim.py:186-192)."""
+    llrs = np.asarray(llrs, np.float64)
+    out = np.empty(llrs.shape)
+    pos = llrs >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-llrs[pos]))
+    e = np.exp(llrs[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def j_counts_from_traces(traces, gammas):
+    """J(gamma) conditioning counts of sim._sim_block (sim.py:172-183):
+    counts[k, gi, 0] = #(correct and D >= gamma), [..., 1] = #(wrong and D >= gamma),
+    D = |p0(total) - p0(pre_total)| per VN at boundary k, correct = total >= 0."""
+    traces = list(traces)
+    n = traces[0].shape[1] // 2
+    out = np.zeros((traces[0].shape[0], len(gammas), 2), np.int64)
+    for tr in traces:
+        for k in range(tr.shape[0]):
+            tot, pre = tr[k, :n], tr[k, n:]
+            d = np.abs(p0_vec(tot) - p0_vec(pre))
+            correct = tot >= 0
+            for gi, gm in enumerate(gammas):
+                sel = d >= gm
+                out[k, gi, 0] += int(np.sum(sel & correct))
+                out[k, gi, 1] += int(np.sum(sel & ~correct))
+    return out
+
+
+def trace_golden_cases():
+    z = np.load(GOLDEN / "trace.npz")
+    return [(si, ast.literal_eval(str(s))) for si, s in enumerate(z["schedules"])]
