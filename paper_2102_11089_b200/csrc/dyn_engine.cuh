@@ -409,7 +409,7 @@ __device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int 
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
 // pre-C2V (and, for CI schedules, pre_total / CI) state.  Leaves the item
 // table of e* for the LMD searches.
-template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G, bool MG = false>
+template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G, bool MG = false, bool TR = false>
 __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
@@ -491,7 +491,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     c.stage[r.w + (r.x - r.y)] = c.in[r.x];
   }
   w.sync();
-  const bool PT = CI || p.pt_on;  // pre_total upkeep (E:171)
+  const bool PT = CI || (TR && p.pt_on);  // pre_total upkeep (E:171); TR: traced build
   const bool dup = PT && g.hop_dup[e_star] != 0;
   // two-hop refresh (E:161-176), G edges per pass in reference order
   for (int base = 0; base < n_items; base += G) {
@@ -709,7 +709,7 @@ __device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, c
 }
 
 // single-edge boundary rule (E:377-384): returns true when decoding stops
-template <typename T, int G>
+template <typename T, int G, bool TR>
 __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c, long long f, bool* conv) {
   if (c.prop != c.next_b) return false;
   c.next_b += p.g.E;
@@ -718,15 +718,15 @@ __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c
   if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
     *conv = true;
     fill_remaining<G>(p, f, k, c.w);
-    trace_rows<T, G>(p, c.total, c.pretot, f, k, true, c.w);
+    if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, k, true, c.w);
     return true;
   }
-  trace_rows<T, G>(p, c.total, c.pretot, f, k, false, c.w);
+  if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, k, false, c.w);
   return false;
 }
 
 // multi-edge boundary rule (E:633-642)
-template <typename T, int G>
+template <typename T, int G, bool TR>
 __device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int* boundary, bool* conv) {
   const long long E = p.g.E;
   while (*boundary <= p.i_max && c.prop >= (long long)(*boundary) * E) {
@@ -735,7 +735,7 @@ __device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int
       *conv = true;
       fill_remaining<G>(p, f, *boundary, c.w);
     }
-    trace_rows<T, G>(p, c.total, c.pretot, f, *boundary, *conv, c.w);
+    if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, *boundary, *conv, c.w);
     ++(*boundary);
     if (*conv) break;
   }
@@ -1078,8 +1078,10 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
 
 // --------------------------------------------------------------- decoders
 
-template <typename T, int KERNEL, bool CI, int G>
-__device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // E:106-127
+// kind: the decode_frame kind (a compile-time constant in per-kind kernels, so
+// the ME-only setup below drops out of the other kernels entirely)
+template <typename T, int KERNEL, bool CI, int G, bool TR = false>
+__device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int kind) {  // E:106-127
   const DevGraph& g = p.g;
   const int lane = c.lane;
   const float* l32 = (const float*)p.llr + f * g.N;
@@ -1097,7 +1099,7 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // 
     for (int e = a; e < b; ++e) c.pre[e] = cn_msg_cached<T, KERNEL>(c.in, a, b, e);
   }
   c.w.sync();
-  if (CI || p.pt_on)
+  if (CI || (TR && p.pt_on))
     for (int n = lane; n < g.N; n += G) {
       T acc = chl(n);
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
@@ -1108,7 +1110,7 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // 
         c.ci[n] = Num<T>::abs_(pt - p0(acc));
       }
     }
-  if (p.fast_sel) {
+  if ((kind == KIND_ME_CIRBP || kind == KIND_ME_LMD_CIRBP) && p.fast_sel) {
     const int W = (g.N + 31) >> 5;
     for (int q = lane; q < p.n_g; q += G) c.hist[q] = 0;
     for (int q = lane; q < p.n_g * W; q += G) c.gbits[q] = 0u;
@@ -1120,12 +1122,12 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f) {  // 
       atomicOr(&c.gbits[gi * W + (n >> 5)], 1u << (n & 31));
     }
   }
-  if (p.kind == KIND_ME_LMD_CIRBP)
+  if (kind == KIND_ME_LMD_CIRBP)
     for (int n = lane; n < g.N; n += G) c.inpp[n] = 0;
   c.w.sync();
 }
 
-template <typename T, int KERNEL, int KF, int G>
+template <typename T, int KERNEL, int KF, int G, bool TR>
 __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
   using Key = typename Num<T>::Key;
@@ -1147,10 +1149,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   }
   const bool ci_kind = kind == KIND_CIRBP || kind == KIND_LMD_CIRBP || kind == KIND_ME_CIRBP ||
                        kind == KIND_ME_LMD_CIRBP;
-  if (ci_kind) init_state<T, KERNEL, true, G>(p, c, f);
-  else init_state<T, KERNEL, false, G>(p, c, f);
+  if (ci_kind) init_state<T, KERNEL, true, G, TR>(p, c, f, kind);
+  else init_state<T, KERNEL, false, G, TR>(p, c, f, kind);
   record_boundary<T, G>(p, c.total, f, 0, c.w);
-  trace_rows<T, G>(p, c.total, c.pretot, f, 0, false, c.w);
+  if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, 0, false, c.w);
   auto rleaf = [&](int e) -> Key { return res_key<T, false, G>(c, e); };
   auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
 
@@ -1160,9 +1162,9 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       while (c.prop < budget) {
         int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
         c.cnt[C_CMP] += E - 1;
-        propagate<T, KERNEL, false, true, false, false, G>(p, c, e);
+        propagate<T, KERNEL, false, true, false, false, G, false, TR>(p, c, e);
         ++c.prop;
-        if (single_boundary<T, G>(p, c, f, &conv)) break;
+        if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
       }
     } break;
     case KIND_CIRBP: {  // E:388-433
@@ -1188,8 +1190,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           e = argmax_vn_edges<T, G>(g, c, n_star);
           c.cnt[C_CMP] += g.vrec[n_star].y - 1;
         }
-        if (flat) propagate<T, KERNEL, true, true, false, false, G>(p, c, e);
-        else propagate<T, KERNEL, true, true, true, false, G>(p, c, e);
+        if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR>(p, c, e);
+        else propagate<T, KERNEL, true, true, true, false, G, false, TR>(p, c, e);
         ++c.prop;
         if (c.prop == c.next_b || c.prop >= budget) {
           if (lane == 0) {
@@ -1198,7 +1200,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           }
           kh = kt = 0;
         }
-        if (single_boundary<T, G>(p, c, f, &conv)) break;
+        if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
       }
     } break;
     case KIND_LMDRBP:
@@ -1207,9 +1209,9 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       int e = argmax_scan<Key>(g.E, c.w, rleaf);
       c.cnt[C_CMP] += E - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, false, false, false, false, G>(p, c, e);
+        int n_items = propagate<T, KERNEL, false, false, false, false, G, false, TR>(p, c, e);
         ++c.prop;
-        if (single_boundary<T, G>(p, c, f, &conv)) break;
+        if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
         int en = lmd_next_edge<T, G>(p, c, e, n_items, simplified);
         if (en < 0) {
@@ -1225,9 +1227,9 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       int e = argmax_vn_edges<T, G>(g, c, n_star);
       c.cnt[C_CMP] += g.vrec[n_star].y - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, true, false, false, false, G>(p, c, e);
+        int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR>(p, c, e);
         ++c.prop;
-        if (single_boundary<T, G>(p, c, f, &conv)) break;
+        if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
         int nn = ci_argmax_twohop<T, G>(p, c, e, n_items, true);
         if (nn < 0) {
@@ -1247,10 +1249,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int pv = c.sel[idx];
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
-          propagate<T, KERNEL, true, false, false, false, G, true>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true, TR>(p, c, e);
           ++c.prop;
         }
-        me_boundaries<T, G>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
       }
     } break;
     case KIND_ME_LMD_CIRBP: {  // E:646-716
@@ -1263,10 +1265,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
           if (lane == 0) c.chosen[idx] = e;
-          propagate<T, KERNEL, true, false, false, false, G, true>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true, TR>(p, c, e);
           ++c.prop;
         }
-        me_boundaries<T, G>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
         if (conv || boundary > I) break;
         // P' = two-hop max-CI VN of each chosen edge, deduplicated in order
         int npc = 0;
@@ -1323,10 +1325,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         c.cnt[C_CMP] += E - 1;
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
-          propagate<T, KERNEL, false, true, false, true, G>(p, c, c.sel[idx]);
+          propagate<T, KERNEL, false, true, false, true, G, false, TR>(p, c, c.sel[idx]);
           ++c.prop;
         }
-        me_boundaries<T, G>(p, c, f, &boundary, &conv);
+        me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
       }
     } break;
     default:
@@ -1351,7 +1353,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
 // MODE 0: E, N and T parts in shared memory; 1: E in HBM, N and T in shared;
 // 2: E and N in HBM, T in shared; 3: everything in HBM.  G lanes per frame
 // (32/G frames per warp); slots and scratch are per frame.
-template <typename T, int KERNEL, int MODE, int KF, int G>
+template <typename T, int KERNEL, int MODE, int KF, int G, bool TR = false>
 __global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int FPW = 32 / G;  // frames per warp
@@ -1404,7 +1406,7 @@ __global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(co
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);
     f = c.w.shfl(f, 0);
     if ((long long)f >= p.B) break;
-    decode_frame<T, KERNEL, KF, G>(p, c, (long long)f);
+    decode_frame<T, KERNEL, KF, G, TR>(p, c, (long long)f);
   }
 }
 

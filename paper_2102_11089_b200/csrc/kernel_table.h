@@ -9,11 +9,21 @@ void* dyn_f64_exact_e_get(int mode, int kind, int g16);
 void* dyn_f64_minsum_get(int mode, int kind, int g16);
 void* dyn_f32_exact_get(int mode, int kind, int g16);
 void* dyn_f32_minsum_get(int mode, int kind, int g16);
+void* dyn_trace_f64_exact_get(int mode);
+void* dyn_trace_f64_minsum_get(int mode);
+void* dyn_trace_f32_exact_get(int mode);
+void* dyn_trace_f32_minsum_get(int mode);
 // float64 + exact kernels are specialised per schedule kind (sLMDRBP runs the
 // LMDRBP kernel); the other variants dispatch on the kind at run time.
 // g16: 16 lanes per frame (two frames per warp; placement modes 1-3 only).
-inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16) {
+// trace: the want_trace build (dyn_trace_*.cu), 32 lanes, kind at run time.
+inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16, int trace = 0) {
   using namespace ldpc;
+  if (trace) {
+    if (g16) return nullptr;
+    if (f64) return kernel == KERNEL_EXACT ? dyn_trace_f64_exact_get(mode) : dyn_trace_f64_minsum_get(mode);
+    return kernel == KERNEL_EXACT ? dyn_trace_f32_exact_get(mode) : dyn_trace_f32_minsum_get(mode);
+  }
   if (g16 && mode == 0) return nullptr;
   if (!f64) return kernel == KERNEL_EXACT ? dyn_f32_exact_get(mode, -1, g16) : dyn_f32_minsum_get(mode, -1, g16);
   if (kernel != KERNEL_EXACT) return dyn_f64_minsum_get(mode, -1, g16);

@@ -158,8 +158,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
 }
 
 template <typename T>
-void* pick_dyn_kernel(int kernel, int mode, int kind, int g16) {
-  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind, g16);
+void* pick_dyn_kernel(int kernel, int mode, int kind, int g16, int trace) {
+  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind, g16, trace);
 }
 
 template <typename T>
@@ -192,7 +192,7 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
     const int fpw = g16 ? 2 : 1;
     const long long per = sh[mode] * fpw;  // shared bytes per warp
     if (per > optin) return c;
-    void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16);
+    void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16, s->want_trace);
     if (!fn) return c;
     int w = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / std::max<long long>(per, 1));
     c.wpb = std::max(1, w);
@@ -389,7 +389,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.ws = (unsigned char*)ws + 256;
     p.tr = tr;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
-    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16);
+    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16, s->want_trace);
     void* args[] = {&p};
     if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,
                                              pl.smem_bytes, st)))
