@@ -56,6 +56,7 @@ struct FixedParams {
   const int* level_tptr;  // [n_levels+1] tile range of each level
   const int* tile_eptr;   // [n_tiles+1] offsets into te_list
   const int* te_list;     // [E] global edge id, tile order
+  const int* te_vn;       // [E] VN of te_list[x] (one load instead of two dependent ones)
   const int2* te_chk;     // [E] tile-local [a, b) of the edge's check
   const int* tile_cptr;   // [n_tiles+1] offsets into tc_rec
   const int4* tc_rec;     // [M] per check in tile order: (local a, degree, first edge id, 0)
@@ -82,58 +83,117 @@ __device__ __forceinline__ T tile_out(const T* in_s, int2 ck, int el, int lane) 
 
 constexpr int kPhaseBRegs = 16;  // checks up to this degree keep their inputs in registers
 
-// All C2V outputs of one check for one frame (lane), inputs from the tile in
-// shared memory.  Exact kernel: prod_q = prefix(in_0..in_{q-1}) continued by
-// in_{q+1}..in_{d-1} -- the reference's left-to-right product (E:55-59) with
-// the prefix shared across outputs.
-template <typename T, int KERNEL, bool LAYERED>
-__device__ __forceinline__ void check_outputs(const DevGraph& g, const T* in_s, const T* old_s, int4 rec,
-                                              int lane, bool act, T* c2v, T* total) {
+// Commit of output q of a check (rec = local a, degree, tile position of its
+// first edge).  c2v rows are stored in tile order (the position in te_list),
+// so a tile's c2v rows are contiguous; layered commits total[vn] = tot + (c2v'
+// - c2v) with tot staged from the tile (tot_s) or re-read (+=).
+template <typename T, bool LAYERED>
+__device__ __forceinline__ void commit_out(const int* te_vn, const T* old_s, const T* tot_s, int la, int ga,
+                                           int q, int lane, T out, T* c2v, T* total) {
   constexpr int F = kFixedFrames;
-  const int la = rec.x, d = rec.y, ga = rec.z;
-  if (d <= kPhaseBRegs) {
-    T in[kPhaseBRegs];
+  c2v[(long long)(ga + q) * F + lane] = out;
+  if (LAYERED) {
+    T* tp = &total[(long long)te_vn[ga + q] * F + lane];
+    const T d_ = out - old_s[(la + q) * F + lane];
+    if (tot_s) *tp = tot_s[(la + q) * F + lane] + d_;
+    else *tp += d_;
+  }
+}
+
+// All C2V outputs of one check of degree D for one frame (lane), inputs from
+// the tile in shared memory, fully unrolled for the degree.  Exact kernel,
+// float64: prod_q = prefix(in_0..in_{q-1}) continued by in_{q+1}..in_{d-1} --
+// the reference's left-to-right product (E:55-59) with the prefix shared.
+// Exact, float32: prefix x suffix (no bit-order obligation in fp32).  Min-sum:
+// min1 / min2 / sign parity in one pass -- the same values as the per-output
+// loop of E:67-82 (min and sign products do not depend on order).
+template <typename T, int KERNEL, bool LAYERED, int D>
+__device__ __forceinline__ void check_outputs_d(const int* te_vn, const T* in_s, const T* old_s, int la, int ga,
+                                                int lane, bool act, T* c2v, T* total, const T* tot_s) {
+  constexpr int F = kFixedFrames;
+  T in[D];
 #pragma unroll
-    for (int q = 0; q < kPhaseBRegs; ++q)
-      if (q < d) in[q] = in_s[(la + q) * F + lane];
-    T pre = T(1);
+  for (int q = 0; q < D; ++q) in[q] = in_s[(la + q) * F + lane];
+  if (KERNEL == KERNEL_EXACT) {
+    constexpr bool kSuffix = sizeof(T) == 4;
+    T suf[D];
+    if (kSuffix) {
+      T acc = T(1);
 #pragma unroll
-    for (int q = 0; q < kPhaseBRegs; ++q) {
-      if (q >= d) break;
-      T out;
-      if (KERNEL == KERNEL_EXACT) {
-        T prod = pre;
-#pragma unroll
-        for (int r = q + 1; r < kPhaseBRegs; ++r)
-          if (r < d) prod *= in[r];
-        out = atanh_msg(prod, d - 1);
-        pre *= in[q];
-      } else {
-        T sign = T(1), mag = Num<T>::kBig;
-#pragma unroll
-        for (int r = 0; r < kPhaseBRegs; ++r) {
-          if (r >= d || r == q) continue;
-          T v = in[r];
-          if (v < T(0)) { sign = -sign; v = -v; }
-          if (v < mag) mag = v;
-        }
-        out = d > 1 ? clampv(sign * mag) : T(0);
-      }
-      if (act) {
-        c2v[(long long)(ga + q) * F + lane] = out;
-        if (LAYERED) total[(long long)g.edge_vn[ga + q] * F + lane] += out - old_s[(la + q) * F + lane];
+      for (int q = D - 1; q >= 0; --q) {
+        suf[q] = acc;
+        acc *= in[q];
       }
     }
-  } else {
-    for (int q = 0; q < d; ++q) {
-      const T out = tile_out<T, KERNEL>(in_s, make_int2(la, la + d), la + q, lane);
-      if (act) {
-        c2v[(long long)(ga + q) * F + lane] = out;
-        if (LAYERED) total[(long long)g.edge_vn[ga + q] * F + lane] += out - old_s[(la + q) * F + lane];
+    T pre = T(1);
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      T prod = pre;
+      if (kSuffix) {
+        prod *= suf[q];
+      } else {
+#pragma unroll
+        for (int r = q + 1; r < D; ++r) prod *= in[r];
       }
+      const T out = atanh_msg(prod, D - 1);
+      pre *= in[q];
+      if (act) commit_out<T, LAYERED>(te_vn, old_s, tot_s, la, ga, q, lane, out, c2v, total);
+    }
+  } else {
+    T m1 = Num<T>::kBig, m2 = Num<T>::kBig, sgn = T(1);
+    int i1 = -1;
+    unsigned negs = 0u;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      T v = clampv(in[q]);
+      if (v < T(0)) {
+        sgn = -sgn;
+        v = -v;
+        negs |= 1u << q;
+      }
+      if (v < m1) {
+        m2 = m1;
+        m1 = v;
+        i1 = q;
+      } else if (v < m2) {
+        m2 = v;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      const T sign = ((negs >> q) & 1u) ? -sgn : sgn;
+      const T out = D > 1 ? clampv(sign * (q == i1 ? m2 : m1)) : T(0);
+      if (act) commit_out<T, LAYERED>(te_vn, old_s, tot_s, la, ga, q, lane, out, c2v, total);
     }
   }
 }
+
+template <typename T, int KERNEL, bool LAYERED>
+__device__ __forceinline__ void check_outputs(const int* te_vn, const T* in_s, const T* old_s, int4 rec, int lane,
+                                              bool act, T* c2v, T* total, const T* tot_s = nullptr) {
+  const int la = rec.x, d = rec.y, ga = rec.z;
+  switch (d) {
+#define LDPC_CK(D_) \
+  case D_: check_outputs_d<T, KERNEL, LAYERED, D_>(te_vn, in_s, old_s, la, ga, lane, act, c2v, total, tot_s); return;
+    LDPC_CK(1) LDPC_CK(2) LDPC_CK(3) LDPC_CK(4) LDPC_CK(5) LDPC_CK(6) LDPC_CK(7) LDPC_CK(8)
+    LDPC_CK(9) LDPC_CK(10) LDPC_CK(11) LDPC_CK(12) LDPC_CK(13) LDPC_CK(14) LDPC_CK(15) LDPC_CK(16)
+#undef LDPC_CK
+    default:
+      for (int q = 0; q < d; ++q) {
+        const T out = tile_out<T, KERNEL>(in_s, make_int2(la, la + d), la + q, lane);
+        if (act) commit_out<T, LAYERED>(te_vn, old_s, tot_s, la, ga, q, lane, out, c2v, total);
+      }
+  }
+}
+
+// Ampere-style asynchronous global->shared copies (LDGSTS), 16 bytes each.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <typename T>
 __device__ __forceinline__ void sign_row(int n, T tv, int k_info, unsigned* sign, int lane, int& errs,
@@ -147,8 +207,14 @@ __device__ __forceinline__ void sign_row(int n, T tv, int k_info, unsigned* sign
   }
 }
 
-template <typename T, int KERNEL, bool LAYERED>
-__global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant__ FixedParams p) {
+// PIPE: the check phase streams tiles through kFixedStages shared-memory
+// stages with cp.async -- tile t+1's c2v and total rows are in flight while
+// tile t computes (within a level; layered levels restart the pipeline because
+// level L+1 reads the totals level L writes).
+constexpr int kFixedStages = 2;
+
+template <typename T, int KERNEL, bool LAYERED, bool PIPE = false>
+__global__ void __launch_bounds__(512, 2) fixed_decode_kernel(const __grid_constant__ FixedParams p) {
   const DevGraph& g = p.g;
   constexpr int F = kFixedFrames;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -159,7 +225,8 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
   unsigned* sign = (unsigned*)(c2v + (long long)g.E * F);
   extern __shared__ __align__(16) unsigned char fixed_smem[];
   T* in_s = (T*)fixed_smem;            // [kTileEdges][32]
-  T* old_s = in_s + kTileEdges * F;    // [kTileEdges][32], layered only
+  T* old_s = in_s + kTileEdges * F;    // [kTileEdges][32], layered only (PIPE: stages follow in_s)
+  T* stg = in_s + kTileEdges * F;      // PIPE: [kFixedStages][2][kTileEdges][32] (c2v rows, total rows)
   __shared__ int s_active[F], s_errs[F], s_errs_info[F], s_iter[F];
   __shared__ unsigned s_unsat;
   __shared__ unsigned long long s_grp;
@@ -233,7 +300,59 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
       if (tid < F) s_errs[tid] = s_errs_info[tid] = 0;
       if (tid == 0) s_unsat = 0;
       // ---- check phase, tile by tile, level by level
-      for (int L = 0; L < p.n_levels; ++L) {
+      if (PIPE) {
+        constexpr int S = kFixedStages;
+        constexpr int CH = F * (int)sizeof(T) / 16;  // 16-byte chunks per row
+        auto stage = [&](int k) { return stg + (long long)k * 2 * kTileEdges * F; };
+        auto issue = [&](int t, int k) {
+          const int ea = p.tile_eptr[t], ne = p.tile_eptr[t + 1] - ea;
+          T* dst = stage(k);
+          for (int x = tid; x < 2 * ne * CH; x += nt) {
+            const int r = x / CH, ch = x - r * CH;
+            const int el = r < ne ? r : r - ne;
+            const T* src = r < ne ? c2v + (long long)(ea + el) * F : total + (long long)p.te_vn[ea + el] * F;
+            cp_async16(dst + ((r < ne ? 0 : kTileEdges) + el) * F + ch * (16 / (int)sizeof(T)),
+                       src + ch * (16 / (int)sizeof(T)));
+          }
+        };
+        for (int L = 0; L < p.n_levels; ++L) {
+          const int t0 = p.level_tptr[L], t1 = p.level_tptr[L + 1];
+          for (int k = 0; k < S - 1; ++k) {
+            if (t0 + k < t1) issue(t0 + k, k);
+            cp_async_commit();
+          }
+          for (int t = t0; t < t1; ++t) {
+            if (t + S - 1 < t1) issue(t + S - 1, (t + S - 1 - t0) % S);
+            cp_async_commit();
+            cp_async_wait<S - 1>();
+            __syncthreads();
+            const int ea = p.tile_eptr[t], ne = p.tile_eptr[t + 1] - ea;
+            const T* so = stage((t - t0) % S);  // c2v rows
+            const T* st = so + kTileEdges * F;  // total rows
+            for (int x = tid; x < ne * F; x += nt) {  // phase A from shared memory
+              const T v = clampv(st[x] - so[x]);
+              in_s[x] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;  // E:58 / E:73
+            }
+            __syncthreads();
+            if (sizeof(T) == 4) {  // one warp per check (shared prefix products)
+              for (int ck = p.tile_cptr[t] + warp; ck < p.tile_cptr[t + 1]; ck += nw)
+                check_outputs<T, KERNEL, LAYERED>(p.te_vn, in_s, so, p.tc_rec[ck], lane, act, c2v, total, st);
+            } else {  // float64: one warp per edge (register-light)
+              for (int el = warp; el < ne; el += nw) {
+                const T out = tile_out<T, KERNEL>(in_s, p.te_chk[ea + el], el, lane);
+                if (act) {
+                  c2v[(long long)(ea + el) * F + lane] = out;
+                  if (LAYERED)
+                    total[(long long)p.te_vn[ea + el] * F + lane] = st[el * F + lane] + (out - so[el * F + lane]);
+                }
+              }
+            }
+            __syncthreads();
+          }
+        }
+        cp_async_wait<0>();
+      }
+      for (int L = 0; L < (PIPE ? 0 : p.n_levels); ++L) {
         for (int t = p.level_tptr[L]; t < p.level_tptr[L + 1]; ++t) {
           const int ea = p.tile_eptr[t], ne = p.tile_eptr[t + 1] - ea;
           // phase A: 4 edges per warp in flight (loads first, then the math)
@@ -243,9 +362,8 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
             for (int u = 0; u < 4; ++u) {
               const int el = el0 + u * nw;
               if (el < ne) {
-                const int e = p.te_list[ea + el];
-                o[u] = c2v[(long long)e * F + lane];
-                tv[u] = total[(long long)g.edge_vn[e] * F + lane];
+                o[u] = c2v[(long long)(ea + el) * F + lane];  // c2v rows in tile order
+                tv[u] = total[(long long)p.te_vn[ea + el] * F + lane];
               }
             }
 #pragma unroll
@@ -262,15 +380,14 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
           if (sizeof(T) == 4) {
             // phase B (float32): one warp per check, inputs in registers, shared prefix
             for (int ck = p.tile_cptr[t] + warp; ck < p.tile_cptr[t + 1]; ck += nw)
-              check_outputs<T, KERNEL, LAYERED>(g, in_s, old_s, p.tc_rec[ck], lane, act, c2v, total);
+              check_outputs<T, KERNEL, LAYERED>(p.te_vn, in_s, old_s, p.tc_rec[ck], lane, act, c2v, total);
           } else {
             // phase B (float64): one warp per edge -- register-light, so twice the warps
             for (int el = warp; el < ne; el += nw) {
-              const int e = p.te_list[ea + el];
               const T out = tile_out<T, KERNEL>(in_s, p.te_chk[ea + el], el, lane);
               if (act) {
-                c2v[(long long)e * F + lane] = out;
-                if (LAYERED) total[(long long)g.edge_vn[e] * F + lane] += out - old_s[el * F + lane];
+                c2v[(long long)(ea + el) * F + lane] = out;
+                if (LAYERED) total[(long long)p.te_vn[ea + el] * F + lane] += out - old_s[el * F + lane];
               }
             }
           }
@@ -285,13 +402,13 @@ __global__ void __launch_bounds__(512) fixed_decode_kernel(const __grid_constant
         if (!LAYERED && act) {
           s = chl[nx];
           const int k0 = g.vn_ptr[n], k1 = g.vn_ptr[n + 1];
-          for (int k = k0; k < k1; k += 4) {  // 4 rows in flight, summed in order (E:749-750)
-            T r[4];
+          for (int k = k0; k < k1; k += 8) {  // 8 rows in flight, summed in order (E:749-750)
+            T r[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
               if (k + u < k1) r[u] = c2v[(long long)g.vn_edges[k + u] * F + lane];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
               if (k + u < k1) s += r[u];
           }
           total[nx] = s;

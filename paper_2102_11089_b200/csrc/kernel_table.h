@@ -37,6 +37,7 @@ inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16, i
   }
 }
 void* ldpc_fixed_kernel(int f64, int kernel, int layered);
+void* ldpc_fixed_pipe_kernel(int f64, int kernel, int layered);  // cp.async-pipelined check phase
 
 namespace ldpc {
 // traced flooding / layered decode (fixed_trace.cu): one warp per frame
@@ -60,3 +61,9 @@ struct FixedTraceParams {
 };
 }  // namespace ldpc
 void* ldpc_fixed_trace_kernel(int f64, int kernel, int layered);
+
+// batch-wide phase kernels for flooding / layered (fixed_phase.cu)
+struct PhaseKernels {
+  void *init, *check, *vn, *syndrome, *finalize, *output;
+};
+PhaseKernels ldpc_phase_kernels(int f64, int kernel, int layered);

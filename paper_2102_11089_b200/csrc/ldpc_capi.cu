@@ -11,15 +11,19 @@
 #include "../../include/ldpc_b200.h"
 #include "dyn_engine.cuh"
 #include "fixed_engine.cuh"
+#define LDPC_PHASE_DECL_ONLY
+#include "fixed_phase.cuh"
 #include "kernel_table.h"
 
 using namespace ldpc;
 
 struct Tiling {  // fixed-engine schedule tiling (see fixed_engine.cuh)
   int n_levels;
+  std::vector<int> h_level_tptr;  // host copy (phase engine launches one check grid per level)
   int* level_tptr;
   int* tile_eptr;
   int* te_list;
+  int* te_vn;
   int2* te_chk;
   int* tile_cptr;
   int4* tc_rec;
@@ -245,9 +249,12 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
 
 struct FixedPlan {
   FixedParams p;
+  void* fn;
   int threads, blocks, smem_bytes;
   long long ws_bytes;
 };
+
+int fixed_engine_choice();
 
 // traced flooding / layered (fixed_trace.cu): one warp per frame, state in HBM
 struct FixedTracePlan {
@@ -278,8 +285,11 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
   const bool layered = s->kind == KIND_LAYERED;
   pl.p.slot_bytes = align16((2ll * G->d.N + G->d.E) * F * sizeof(T) + 4ll * G->d.N);
   pl.threads = 512;
-  pl.smem_bytes = (layered ? 2 : 1) * kTileEdges * F * (int)sizeof(T);
-  void* fn = pick_fixed_kernel<T>(s->kernel, layered);
+  const bool pipe = fixed_engine_choice() == 2;
+  pl.smem_bytes = (pipe ? 1 + 2 * kFixedStages : (layered ? 2 : 1)) * kTileEdges * F * (int)sizeof(T);
+  if (pl.smem_bytes > smem_optin() - 1024) return LDPC_ERR_UNSUPPORTED;
+  void* fn = pipe ? ldpc_fixed_pipe_kernel(sizeof(T) == 8, s->kernel, layered) : pick_fixed_kernel<T>(s->kernel, layered);
+  pl.fn = fn;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.threads, pl.smem_bytes) != cudaSuccess || occ < 1) occ = 1;
@@ -295,9 +305,133 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
   pl.p.level_tptr = tl.level_tptr;
   pl.p.tile_eptr = tl.tile_eptr;
   pl.p.te_list = tl.te_list;
+  pl.p.te_vn = tl.te_vn;
   pl.p.te_chk = tl.te_chk;
   pl.p.tile_cptr = tl.tile_cptr;
   pl.p.tc_rec = tl.tc_rec;
+  return LDPC_OK;
+}
+
+// ------------------------------------------------- fixed schedules, phase engine
+
+// Engine choice for flooding / layered: "phase" (batch-wide phases, default),
+// "tile" (one persistent CTA per 32-frame group), "pipe" (tile + cp.async).
+int fixed_engine_choice() {
+  const char* e = getenv("LDPC_FIXED_ENGINE");
+  if (!e) return 0;
+  if (!strcmp(e, "tile")) return 1;
+  if (!strcmp(e, "pipe")) return 2;
+  return 0;
+}
+
+struct PhasePlan {
+  long long slot, sign_off, groups, chunk, state_off, ws_bytes;
+  int smem_check;
+};
+
+template <typename T>
+int phase_plan(const ldpc_graph* G, long long B, PhasePlan& pl) {
+  const long long F = kFixedFrames, N = G->d.N, E = G->d.E;
+  pl.sign_off = align16((2 * N + E) * F * (long long)sizeof(T));
+  pl.slot = align16(pl.sign_off + 4 * N);
+  pl.groups = (B + F - 1) / F;
+  const long long per_group_state = 4 + 4 + 3 * 4 * F;  // amask, unsat, errs, errs_info, iters
+  pl.chunk = std::max<long long>(1, std::min(pl.groups, (24ll << 30) / (pl.slot + per_group_state)));
+  pl.state_off = 256 + pl.chunk * pl.slot;
+  pl.ws_bytes = pl.state_off + align16(pl.chunk * per_group_state) + 64;
+  pl.smem_check = 3 * kTileEdges * (int)F * (int)sizeof(T);
+  return LDPC_OK;
+}
+
+template <typename T>
+int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_sched_t* s, int8_t* u_hat,
+                 int64_t* props, uint8_t* conv, int64_t* counters, int32_t* biterr, int32_t* biterr_info,
+                 void* ws, size_t ws_bytes, cudaStream_t st) {
+  PhasePlan pl;
+  phase_plan<T>(G, B, pl);
+  if ((long long)ws_bytes < pl.ws_bytes) return LDPC_ERR_WORKSPACE;
+  const bool layered = s->kind == KIND_LAYERED;
+  const PhaseKernels K = ldpc_phase_kernels(sizeof(T) == 8, s->kernel, layered);
+  const Tiling& tl = layered ? G->layer : G->flood;
+  const std::vector<int>& lvl = tl.h_level_tptr;
+  cudaFuncSetAttribute(K.check, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_check);
+  auto grid_of = [&](void* fn, int smem, long long items) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPhaseThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return (int)std::max<long long>(1, std::min<long long>((long long)occ * sm_count(), items));
+  };
+  const int I = s->i_max;
+  int launches = 0;
+  for (long long g0 = 0; g0 < pl.groups; g0 += pl.chunk) {
+    PhaseParams p;
+    memset(&p, 0, sizeof(p));
+    p.g = G->d;
+    p.kernel = s->kernel;
+    p.i_max = I;
+    p.k_info = s->k_info;
+    p.llr = llr;
+    p.llr_f64 = s->llr_f64;
+    p.f_base = g0 * kFixedFrames;
+    p.B = std::min<long long>(B - p.f_base, pl.chunk * kFixedFrames);
+    p.groups = (int)((p.B + kFixedFrames - 1) / kFixedFrames);
+    p.u_hat = u_hat;
+    p.prop = (long long*)props;
+    p.conv = conv;
+    p.counters = (long long*)counters;
+    p.biterr = biterr;
+    p.biterr_info = biterr_info;
+    p.ws = (unsigned char*)ws + 256;
+    p.slot_bytes = pl.slot;
+    p.sign_off = pl.sign_off;
+    unsigned char* sb = (unsigned char*)ws + pl.state_off;
+    p.amask = (unsigned*)sb;
+    p.unsat = p.amask + pl.chunk;
+    p.errs = (int*)(p.unsat + pl.chunk);
+    p.errs_info = p.errs + pl.chunk * kFixedFrames;
+    p.iters = p.errs_info + pl.chunk * kFixedFrames;
+    p.level_tptr = tl.level_tptr;
+    p.tile_eptr = tl.tile_eptr;
+    p.te_list = tl.te_list;
+    p.te_vn = tl.te_vn;
+    p.te_chk = tl.te_chk;
+    p.tile_cptr = tl.tile_cptr;
+    p.tc_rec = tl.tc_rec;
+    if (int rc = cuda_check(cudaMemsetAsync(p.errs, 0, 2ll * pl.chunk * kFixedFrames * 4, st))) return rc;
+    const long long G_ = p.groups;
+    const long long vch = (G->d.N + kPhaseVnChunk - 1) / kPhaseVnChunk;
+    const long long ech = ((long long)G->d.E + kPhaseVnChunk * 8 - 1) / (kPhaseVnChunk * 8);
+    const long long cch = (G->d.M + kPhaseChkChunk - 1) / kPhaseChkChunk;
+    auto launch = [&](void* fn, long long items, int smem, void** args, int threads = kPhaseThreads) {
+      ++launches;
+      const int grid = threads == kPhaseThreads ? grid_of(fn, smem, items) : (int)items;
+      return cuda_check(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, st));
+    };
+    void* a1[] = {&p};
+    int k = 0, chk = 0;
+    void* af[] = {&p, &k, &chk};
+    const long long fin_blocks = (G_ * kFixedFrames + 255) / 256;
+    if (int rc = launch(K.init, G_ * (vch + ech), 0, a1)) return rc;
+    if (I == 0)
+      if (int rc = launch(K.syndrome, G_ * cch, 0, a1)) return rc;
+    k = 0;
+    chk = I == 0 ? 1 : 0;
+    if (int rc = launch(K.finalize, fin_blocks, 0, af, 256)) return rc;
+    for (int it = 1; it <= I; ++it) {
+      for (int L = 0; L < tl.n_levels; ++L) {
+        int t_lo = lvl[L], t_hi = lvl[L + 1];
+        if (t_hi <= t_lo) continue;
+        void* ac[] = {&p, &t_lo, &t_hi};
+        if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) return rc;
+      }
+      if (int rc = launch(K.vn, G_ * vch, 0, a1)) return rc;
+      if (int rc = launch(K.syndrome, G_ * cch, 0, a1)) return rc;
+      k = it;
+      chk = 1;
+      if (int rc = launch(K.finalize, fin_blocks, 0, af, 256)) return rc;
+    }
+    if (int rc = launch(K.output, G_ * vch, 0, a1)) return rc;
+  }
+  g_last_launches = launches;
   return LDPC_OK;
 }
 
@@ -395,6 +529,8 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
                                              pl.smem_bytes, st)))
       return rc;
     g_last_launches = 1;
+  } else if (fixed_engine_choice() == 0) {
+    return phase_decode<T>(G, llr, B, s, u_hat, props, conv, counters, biterr, biterr_info, ws, ws_bytes, st);
   } else {
     FixedPlan pl;
     if (int rc = fixed_plan<T>(G, s, B, pl)) return rc;
@@ -418,9 +554,8 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.ws = (unsigned char*)ws + 256;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
     if (int rc = cuda_check(cudaMemsetAsync(conv, 0, B, st))) return rc;
-    void* fn = pick_fixed_kernel<T>(s->kernel, s->kind == KIND_LAYERED);
     void* args[] = {&p};
-    if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.threads), args, pl.smem_bytes, st)))
+    if (int rc = cuda_check(cudaLaunchKernel(pl.fn, dim3(pl.blocks), dim3(pl.threads), args, pl.smem_bytes, st)))
       return rc;
     g_last_launches = 1;
   }
@@ -557,12 +692,14 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
           t.tile_cptr.push_back((int)t.tc_rec.size() / 4);
           cur = 0;
         }
+        // (local a, degree, tile-order position of the first edge): c2v rows
+        // live in tile order; the flooding tiling is the identity order
+        t.tc_rec.insert(t.tc_rec.end(), {cur, d, (int)t.te_list.size(), 0});
         for (int e = cn_ptr[m]; e < cn_ptr[m + 1]; ++e) {
           t.te_list.push_back(e);
           t.te_chk.push_back(cur);
           t.te_chk.push_back(cur + d);
         }
-        t.tc_rec.insert(t.tc_rec.end(), {cur, d, cn_ptr[m], 0});
         cur += d;
       }
       if (cur > 0) {
@@ -689,7 +826,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
   {
     size_t tot = 0;
     for (auto& t : ht)
-      tot += t.level_tptr.size() + t.tile_eptr.size() + t.te_list.size() + t.te_chk.size() + t.tile_cptr.size() +
+      tot += t.level_tptr.size() + t.tile_eptr.size() + 2 * t.te_list.size() + t.te_chk.size() + t.tile_cptr.size() +
              t.tc_rec.size() + 8;
     int* tb = nullptr;
     if (cudaMalloc(&tb, tot * sizeof(int)) != cudaSuccess) {
@@ -713,6 +850,8 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       hb.insert(hb.end(), t.tile_eptr.begin(), t.tile_eptr.end());
       size_t o_tl = hb.size();
       hb.insert(hb.end(), t.te_list.begin(), t.te_list.end());
+      size_t o_vn = hb.size();
+      for (int e : t.te_list) hb.push_back(edge_vn[e]);
       size_t o_cp = hb.size();
       hb.insert(hb.end(), t.tile_cptr.begin(), t.tile_cptr.end());
       dst[i]->tc_rec = (int4*)(tb + o_rec);
@@ -722,6 +861,8 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       dst[i]->level_tptr = tb + o_lt;
       dst[i]->tile_eptr = tb + o_te;
       dst[i]->te_list = tb + o_tl;
+      dst[i]->te_vn = tb + o_vn;
+      dst[i]->h_level_tptr = t.level_tptr;
     }
     if (cudaMemcpy(tb, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
       cudaFree(tb);
@@ -824,6 +965,11 @@ int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B,
       FixedTracePlan pl;
       int rc = s->precision == LDPC_F64 ? fixed_trace_plan<double>(G, s, B, pl) : fixed_trace_plan<float>(G, s, B, pl);
       if (rc) return rc;
+      ws = pl.ws_bytes;
+    } else if (fixed_engine_choice() == 0) {
+      PhasePlan pl;
+      if (s->precision == LDPC_F64) phase_plan<double>(G, B, pl);
+      else phase_plan<float>(G, B, pl);
       ws = pl.ws_bytes;
     } else {
       FixedPlan pl;

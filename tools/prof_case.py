@@ -21,7 +21,10 @@ placement = next((f for f in flags if f in ("smem", "split", "hbm", "trees")), "
 prec = "f32" if "f32" in flags else "f64"
 n_p = 4
 imax_over = None
+max_res = 0
 for f in flags:
+    if f.startswith("res="):
+        max_res = int(f[4:])
     if f.startswith("n_p="):
         n_p = int(f[4:])
     if f.startswith("imax="):
@@ -34,12 +37,16 @@ if key == "C4":
 llr = torch.from_numpy(llr_batch(spec, eb, 0, 0, nfr)).cuda()
 imax = imax_over or imax
 cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=n_p, precision=prec)
-decode_batch(spec, llr[:1], cfg, placement=placement)
+decode_batch(spec, llr[:1], cfg, placement=placement, max_resident=max_res)
 torch.cuda.synchronize()
-t = time.time()
-out = decode_batch(spec, llr, cfg, placement=placement)
-torch.cuda.synchronize()
-dt = time.time() - t
+reps = int(next((f[5:] for f in flags if f.startswith("reps=")), "1"))
+dts = []
+for _ in range(reps):  # ncu: -s 1 -c 1 captures the first of these
+    t = time.time()
+    out = decode_batch(spec, llr, cfg, placement=placement, max_resident=max_res)
+    torch.cuda.synchronize()
+    dts.append(time.time() - t)
+dt = min(dts)
 upd = int(out["counters"][:, 0].sum())
-print(f"{key} {kind} {prec} {placement} frames={nfr} time={dt*1e3:.2f} ms updates={upd} "
+print(f"{key} {kind} {prec} {placement} res={max_res} frames={nfr} time={dt*1e3:.2f} ms updates={upd} "
       f"upd/s={upd/dt:.3e} frames/s={nfr/dt:.3e} us/update/warp-est={dt*1e6/max(1,upd/nfr):.2f}")
