@@ -53,6 +53,17 @@ struct PhaseParams {
   const int2* te_chk;
   const int* tile_cptr;
   const int4* tc_rec;
+  // strips (fixed_tma.cuh): s_rec[t] = (first c2v row, k checks, degree d, first run),
+  // s_runs = (first VN, staged row | length << 8), s_vn = VN of each staged row
+  const int4* s_rec;
+  const int2* s_runs;
+  const int* s_vn;
+  const int* vn_rows;  // [E] c2v row of each vn_edges slot (VN phase)
+  // VN strips (flooding VN phase, fixed_tma.cuh): v_rec[t] = (first VN, k, degree, first run),
+  // v_runs = (first stored c2v row, staged row | length << 8)
+  const int4* v_rec;
+  const int2* v_runs;
+  int n_vstrips;
 };
 
 #ifndef LDPC_PHASE_DECL_ONLY  // the host launcher only needs PhaseParams
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_vn_kernel(const __grid_co
           T r[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (k + u < k1) r[u] = s.c2v[(long long)g.vn_edges[k + u] * F + lane];
+            if (k + u < k1) r[u] = s.c2v[(long long)p.vn_rows[k + u] * F + lane];
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             if (k + u < k1) v += r[u];
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_vn_kernel(const __grid_co
 }
 
 // Parity of every check from the sign words, 32 frames per word (E:179-188).
-__global__ void __launch_bounds__(kPhaseThreads) phase_syndrome_kernel(const __grid_constant__ PhaseParams p) {
+static __global__ void __launch_bounds__(kPhaseThreads) phase_syndrome_kernel(const __grid_constant__ PhaseParams p) {
   const DevGraph& g = p.g;
   const int cchunks = (g.M + kPhaseChkChunk - 1) / kPhaseChkChunk;
   const long long items = (long long)p.groups * cchunks;
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_syndrome_kernel(const __g
 }
 
 // Boundary k: record bit errors, retire converged frames (k > 0), reset tallies.
-__global__ void phase_finalize_kernel(const __grid_constant__ PhaseParams p, int k, int check) {
+static __global__ void phase_finalize_kernel(const __grid_constant__ PhaseParams p, int k, int check) {
   constexpr int F = kFixedFrames;
   const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= (long long)p.groups * F) return;
@@ -302,3 +313,5 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_output_kernel(const __gri
 #endif  // LDPC_PHASE_DECL_ONLY
 
 }  // namespace ldpc
+
+#include "fixed_tma.cuh"  // TMA-fed check phase (uses PhaseParams / GroupSlot)

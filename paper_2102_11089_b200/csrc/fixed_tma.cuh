@@ -1,0 +1,439 @@
+// fixed_tma.cuh -- warp-specialised, TMA-fed check phase for flooding / layered.
+//
+// Same work as phase_check_kernel (fixed_phase.cuh): every (32-frame group,
+// strip) item of one level gets its C2V outputs (E:49-103 arithmetic, the
+// reference's operation order in float64) and, for layered, its total commits.
+//
+// Strips (built on the host, ldpc_capi.cu): k consecutive checks of one level
+// with the same degree d (k*d <= kTileEdges), staged SLOT-MAJOR -- row q*k + c
+// holds slot q (the q-th edge, ascending VN) of check c.  The c2v rows of the
+// flooding / layered schedules are STORED in that order too, so a strip's c2v
+// rows are one contiguous block, and for quasi-cyclic codes (a block row's Z
+// checks have the same degree; slot q of consecutive checks hits consecutive
+// VNs of one circulant) the gathered total rows of a slot are a few contiguous
+// VN runs.  The host stores those runs per strip.
+//
+// Pipeline (kTmaStages shared-memory stages, transaction mbarriers):
+//   * one producer warp streams items: one bulk async copy (cp.async.bulk, the
+//     TMA engine) for the strip's c2v block and one per total-row run, so a
+//     BG1 strip of ~120 edges costs ~8-14 copy instructions instead of 256
+//     row gathers.  The next item's strip record and runs are loaded into
+//     registers while the current item's copies fly;
+//   * consumer warps take whole checks of the staged strip: they form the
+//     check inputs tanh(clamp(total - c2v)/2) (or the V2C for min-sum) from
+//     the staged rows into registers, compute all outputs, store each output
+//     row (one coalesced 32-frame row per warp store) and release the stage
+//     through an "empty" mbarrier.  No CTA-wide barrier in the steady state.
+#pragma once
+#include "fixed_engine.cuh"
+
+namespace ldpc {
+
+constexpr int kTmaStages = 3;
+
+template <typename T, int NC>
+struct TmaLayout {
+  static constexpr int F = kFixedFrames;
+  static constexpr int kRows = kTileEdges * F;              // elements of one row block
+  static constexpr int kRowBytes = F * (int)sizeof(T);      // one 32-frame row
+  static constexpr int kStageBytes = 2 * kRows * (int)sizeof(T) + kTileEdges * 4;
+  static constexpr int kBarOff = kTmaStages * kStageBytes;  // 2 x kTmaStages mbarriers
+  static constexpr int kBytes = kBarOff + 2 * kTmaStages * 8;
+  static constexpr int kThreads = (NC + 1) * 32;
+  static constexpr int kMinBlocks = sizeof(T) == 4 ? 2 : 1;
+};
+
+// VN phase (flooding): VN strips of k consecutive VNs with the same degree dv,
+// staged rows [s*k + v] = c2v of the v-th VN's s-th edge (vn_edges order),
+// then k chl rows.  k*dv <= kTileEdges, k <= kVnStripMax.
+constexpr int kVnStripMax = 64;
+template <typename T, int NC>
+struct VnLayout {
+  static constexpr int F = kFixedFrames;
+  static constexpr int kRowsMax = kTileEdges + kVnStripMax;
+  static constexpr int kRowBytes = F * (int)sizeof(T);
+  static constexpr int kStageBytes = kRowsMax * kRowBytes;
+  static constexpr int kBarOff = kTmaStages * kStageBytes;
+  static constexpr int kBytes = kBarOff + 2 * kTmaStages * 8;
+  static constexpr int kThreads = (NC + 1) * 32;
+};
+
+// ----------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  while (!mbar_try(b, parity)) {
+  }
+}
+// global -> shared bulk copy (TMA engine), completion counted on mbarrier `b`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+// ------------------------------------------------------ fused check math
+// Input of staged row x: tanh(clamp(total - c2v)/2) (E:58) or the clamped V2C
+// (min-sum, E:73).
+template <typename T, int KERNEL>
+__device__ __forceinline__ T staged_in(const T* so, const T* st, int x) {
+  const T v = clampv(st[x] - so[x]);
+  return (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+}
+
+// Output of staged row r (lane = frame): c2v row e0 + r; layered also commits
+// total[vn] = total_old + (c2v_new - c2v_old).
+template <typename T, bool LAYERED>
+__device__ __forceinline__ void strip_commit(const T* so, const T* st, const int* tv, int r, long long e0, int lane,
+                                             T out, T* c2v, T* total) {
+  constexpr int F = kFixedFrames;
+  c2v[(e0 + r) * F + lane] = out;
+  if (LAYERED) total[(long long)tv[r] * F + lane] = st[r * F + lane] + (out - so[r * F + lane]);
+}
+
+// All outputs of check c of a strip (k checks of degree D, slot-major rows).
+// float64 keeps the reference's left-to-right product (shared prefix, then
+// the remaining inputs in order); float32 uses prefix x suffix.  Min-sum:
+// min1 / min2 / sign parity (order-free, same values as E:67-82).
+template <typename T, int KERNEL, bool LAYERED, int D>
+__device__ __forceinline__ void strip_check_d(const T* so, const T* st, const int* tv, int c, int k, long long e0,
+                                              int lane, T* c2v, T* total) {
+  constexpr int F = kFixedFrames;
+  T in[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) in[q] = staged_in<T, KERNEL>(so, st, (q * k + c) * F + lane);
+  if (KERNEL == KERNEL_EXACT) {
+    constexpr bool kSuffix = sizeof(T) == 4;
+    T suf[D];
+    if (kSuffix) {
+      T acc = T(1);
+#pragma unroll
+      for (int q = D - 1; q >= 0; --q) {
+        suf[q] = acc;
+        acc *= in[q];
+      }
+    }
+    T pre = T(1);
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      T prod = pre;
+      if (kSuffix) {
+        prod *= suf[q];
+      } else {
+#pragma unroll
+        for (int r = q + 1; r < D; ++r) prod *= in[r];
+      }
+      pre *= in[q];
+      strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, atanh_msg(prod, D - 1), c2v, total);
+    }
+  } else {
+    T m1 = Num<T>::kBig, m2 = Num<T>::kBig, sgn = T(1);
+    int i1 = -1;
+    unsigned negs = 0u;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      T v = in[q];
+      if (v < T(0)) {
+        sgn = -sgn;
+        v = -v;
+        negs |= 1u << q;
+      }
+      if (v < m1) {
+        m2 = m1;
+        m1 = v;
+        i1 = q;
+      } else if (v < m2) {
+        m2 = v;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      const T sign = ((negs >> q) & 1u) ? -sgn : sgn;
+      const T out = D > 1 ? clampv(sign * (q == i1 ? m2 : m1)) : T(0);
+      strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, out, c2v, total);
+    }
+  }
+}
+
+// Degrees above the unrolled range: each output recomputes its inputs in the
+// reference's order (O(d^2) transcendental work; such checks are rare).
+template <typename T, int KERNEL, bool LAYERED>
+__device__ __noinline__ void strip_check_generic(const T* so, const T* st, const int* tv, int c, int k, int d,
+                                                 long long e0, int lane, T* c2v, T* total) {
+  constexpr int F = kFixedFrames;
+  for (int q = 0; q < d; ++q) {
+    T out;
+    if (KERNEL == KERNEL_EXACT) {
+      T prod = T(1);
+      for (int r = 0; r < d; ++r)
+        if (r != q) prod *= staged_in<T, KERNEL>(so, st, (r * k + c) * F + lane);
+      out = atanh_msg(prod, d - 1);
+    } else {
+      T sign = T(1), mag = Num<T>::kBig;
+      for (int r = 0; r < d; ++r) {
+        if (r == q) continue;
+        T v = staged_in<T, KERNEL>(so, st, (r * k + c) * F + lane);
+        if (v < T(0)) {
+          sign = -sign;
+          v = -v;
+        }
+        if (v < mag) mag = v;
+      }
+      out = d > 1 ? clampv(sign * mag) : T(0);
+    }
+    strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, out, c2v, total);
+  }
+}
+
+// The checks c = c0, c0 + step, ... of a staged strip (k checks, degree d).
+template <typename T, int KERNEL, bool LAYERED>
+__device__ __forceinline__ void strip_checks(const T* so, const T* st, const int* tv, int c0, int step, int k, int d,
+                                             long long e0, int lane, T* c2v, T* total) {
+  switch (d) {
+#define LDPC_SCK(D_)                                                                           \
+  case D_:                                                                                     \
+    for (int c = c0; c < k; c += step) strip_check_d<T, KERNEL, LAYERED, D_>(so, st, tv, c, k, e0, lane, c2v, total); \
+    return;
+    LDPC_SCK(1) LDPC_SCK(2) LDPC_SCK(3) LDPC_SCK(4) LDPC_SCK(5) LDPC_SCK(6) LDPC_SCK(7) LDPC_SCK(8)
+    LDPC_SCK(9) LDPC_SCK(10) LDPC_SCK(11) LDPC_SCK(12) LDPC_SCK(13) LDPC_SCK(14) LDPC_SCK(15) LDPC_SCK(16)
+#undef LDPC_SCK
+    default:
+      for (int c = c0; c < k; c += step) strip_check_generic<T, KERNEL, LAYERED>(so, st, tv, c, k, d, e0, lane, c2v, total);
+  }
+}
+
+#ifndef LDPC_PHASE_DECL_ONLY
+
+// Check phase over the strips [t_lo, t_hi) of one level, all active groups.
+// Block = NC consumer warps + 1 producer warp (the last one).
+template <typename T, int KERNEL, bool LAYERED, int NC>
+__global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::kMinBlocks)
+    phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int t_lo, int t_hi) {
+  using L = TmaLayout<T, NC>;
+  constexpr int F = kFixedFrames, S = kTmaStages, RPL = kTileEdges / 32;  // runs / rows per lane
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  auto so_of = [&](int s) { return (T*)(tma_smem + s * L::kStageBytes); };
+  auto st_of = [&](int s) { return (T*)(tma_smem + s * L::kStageBytes) + L::kRows; };
+  auto tv_of = [&](int s) { return (int*)(tma_smem + s * L::kStageBytes + 2 * L::kRows * (int)sizeof(T)); };
+  unsigned long long* full = (unsigned long long*)(tma_smem + L::kBarOff);
+  unsigned long long* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int nti = t_hi - t_lo;
+  const long long items = (long long)p.groups * nti;
+
+  if (warp == NC) {  // ---------------- producer
+    auto seek = [&](long long i) {
+      for (; i < items; i += gridDim.x)
+        if (p.amask[i / nti]) break;
+      return i;
+    };
+    long long it = seek(blockIdx.x);
+    int4 rec = make_int4(0, 0, 0, 0);
+    int nrun = 0;
+    int2 run[RPL];
+    int vn[RPL];
+    auto prefetch = [&](long long i) {
+      if (i >= items) return;
+      const int t = t_lo + (int)(i % nti);
+      rec = p.s_rec[t];
+      nrun = p.s_rec[t + 1].w - rec.w;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const int r = lane + 32 * j;
+        if (r < nrun) run[j] = p.s_runs[rec.w + r];
+        if (LAYERED && r < rec.y * rec.z) vn[j] = p.s_vn[rec.x + r];
+      }
+    };
+    prefetch(it);
+    for (int kk = 0; it < items; ++kk) {
+      const int s = kk % S;
+      const unsigned u = (unsigned)(kk / S);
+      if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
+      GroupSlot<T> gs(p, it / nti);
+      const int rows = rec.y * rec.z;
+      if (LAYERED) {
+        int* tv = tv_of(s);
+#pragma unroll
+        for (int j = 0; j < RPL; ++j)
+          if (lane + 32 * j < rows) tv[lane + 32 * j] = vn[j];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_tx(&full[s], 2u * rows * L::kRowBytes);
+        bulk_g2s(so_of(s), gs.c2v + (long long)rec.x * F, rows * L::kRowBytes, &full[s]);
+      }
+      __syncwarp();
+      T* st = st_of(s);
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        if (lane + 32 * j < nrun) {
+          const int row = run[j].y & 0xff, len = run[j].y >> 8;
+          bulk_g2s(st + row * F, gs.total + (long long)run[j].x * F, len * L::kRowBytes, &full[s]);
+        }
+      }
+      it = seek(it + gridDim.x);
+      prefetch(it);
+    }
+  } else {  // ---------------- consumers
+    long long it = blockIdx.x;
+    for (int kk = 0; it < items; it += gridDim.x) {
+      const long long grp = it / nti;
+      const unsigned am = p.amask[grp];
+      if (!am) continue;
+      const int s = kk % S;
+      const unsigned u = (unsigned)(kk / S);
+      ++kk;
+      const int4 rec = p.s_rec[t_lo + (int)(it - grp * nti)];
+      GroupSlot<T> gs(p, grp);
+      mbar_wait(&full[s], u & 1u);
+      if ((am >> lane) & 1u)
+        strip_checks<T, KERNEL, LAYERED>(so_of(s), st_of(s), tv_of(s), warp, NC, rec.y, rec.z, rec.x, lane, gs.c2v,
+                                         gs.total);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+}
+
+
+// VN phase of flooding over VN strips (E:746-756): total = chl + the C2V of
+// the VN's edges in vn_edges order (the reference's summation order), sign
+// words, error tallies.  Producer: one bulk copy of the strip's chl rows and
+// one per run of consecutive stored c2v rows.  Consumers: one VN per warp.
+template <typename T, int NC>
+__global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 : 1)
+    phase_vn_tma_kernel(const __grid_constant__ PhaseParams p) {
+  using L = VnLayout<T, NC>;
+  constexpr int F = kFixedFrames, S = kTmaStages, RPL = kTileEdges / 32;
+  extern __shared__ __align__(128) unsigned char vn_smem[];
+  auto stage = [&](int s) { return (T*)(vn_smem + s * L::kStageBytes); };
+  unsigned long long* full = (unsigned long long*)(vn_smem + L::kBarOff);
+  unsigned long long* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int nvs = p.n_vstrips;
+  const long long items = (long long)p.groups * nvs;
+  if (warp == NC) {  // ---------------- producer
+    auto seek = [&](long long i) {
+      for (; i < items; i += gridDim.x)
+        if (p.amask[i / nvs]) break;
+      return i;
+    };
+    long long it = seek(blockIdx.x);
+    int4 rec = make_int4(0, 0, 0, 0);
+    int nrun = 0;
+    int2 run[RPL];
+    auto prefetch = [&](long long i) {
+      if (i >= items) return;
+      const int t = (int)(i % nvs);
+      rec = p.v_rec[t];
+      nrun = p.v_rec[t + 1].w - rec.w;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j)
+        if (lane + 32 * j < nrun) run[j] = p.v_runs[rec.w + lane + 32 * j];
+    };
+    prefetch(it);
+    for (int kk = 0; it < items; ++kk) {
+      const int s = kk % S;
+      const unsigned u = (unsigned)(kk / S);
+      if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
+      GroupSlot<T> gs(p, it / nvs);
+      const int k = rec.y, erows = k * rec.z;
+      T* sb = stage(s);
+      if (lane == 0) {
+        mbar_arrive_tx(&full[s], (unsigned)(erows + k) * L::kRowBytes);
+        bulk_g2s(sb + erows * F, gs.chl + (long long)rec.x * F, k * L::kRowBytes, &full[s]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        if (lane + 32 * j < nrun) {
+          const int row = run[j].y & 0xff, len = run[j].y >> 8;
+          bulk_g2s(sb + row * F, gs.c2v + (long long)run[j].x * F, len * L::kRowBytes, &full[s]);
+        }
+      }
+      it = seek(it + gridDim.x);
+      prefetch(it);
+    }
+  } else {  // ---------------- consumers
+    long long it = blockIdx.x;
+    for (int kk = 0; it < items; it += gridDim.x) {
+      const long long grp = it / nvs;
+      const unsigned am = p.amask[grp];
+      if (!am) continue;
+      const int s = kk % S;
+      const unsigned u = (unsigned)(kk / S);
+      ++kk;
+      const int4 rec = p.v_rec[(int)(it - grp * nvs)];
+      GroupSlot<T> gs(p, grp);
+      const bool act = (am >> lane) & 1u;
+      const int k = rec.y, dv = rec.z;
+      mbar_wait(&full[s], u & 1u);
+      const T* sb = stage(s);
+      int errs = 0, ei = 0;
+      for (int v = warp; v < k; v += NC) {
+        const int n = rec.x + v;
+        T tv;
+        if (act) {
+          tv = sb[(k * dv + v) * F + lane];  // chl
+          for (int q = 0; q < dv; ++q) tv += sb[(q * k + v) * F + lane];
+          gs.total[(long long)n * F + lane] = tv;
+        } else {
+          tv = gs.total[(long long)n * F + lane];
+        }
+        int e_ = 0, i_ = 0;
+        sign_row<T>(n, tv, p.k_info, gs.sign, lane, e_, i_);
+        if (act) {
+          errs += e_;
+          ei += i_;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (errs) atomicAdd(&p.errs[grp * F + lane], errs);
+      if (ei) atomicAdd(&p.errs_info[grp * F + lane], ei);
+    }
+  }
+}
+
+#endif  // LDPC_PHASE_DECL_ONLY
+
+}  // namespace ldpc

@@ -65,5 +65,11 @@ void* ldpc_fixed_trace_kernel(int f64, int kernel, int layered);
 // batch-wide phase kernels for flooding / layered (fixed_phase.cu)
 struct PhaseKernels {
   void *init, *check, *vn, *syndrome, *finalize, *output;
+  void* check_tma;           // warp-specialised TMA-fed check phase (fixed_tma.cuh)
+  int tma_threads, tma_smem;
+  void* vn_tma;              // TMA-fed VN phase over VN strips (flooding)
+  int vn_threads, vn_smem;
 };
 PhaseKernels ldpc_phase_kernels(int f64, int kernel, int layered);
+void ldpc_phase_fill_f64(PhaseKernels& k, int kernel, int layered);  // fixed_phase_f64.cu
+void ldpc_phase_fill_f32(PhaseKernels& k, int kernel, int layered);  // fixed_phase_f32.cu

@@ -29,11 +29,24 @@ struct Tiling {  // fixed-engine schedule tiling (see fixed_engine.cuh)
   int4* tc_rec;
 };
 
+struct Strips {  // slot-major check strips of the TMA-fed check phase (fixed_tma.cuh)
+  std::vector<int> h_level_sptr;  // strip range of each level (host copy)
+  int4* rec;                      // [n_strips + 1] (first c2v row, k, d, first run); sentinel .x/.w = totals
+  int2* runs;                     // (first VN, staged row | length << 8)
+  int* vn;                        // [E] VN of each staged / stored row
+  int* vn_rows;                   // [E] stored c2v row of each vn_edges slot
+  int n_vstrips;                  // VN strips (flooding VN phase)
+  int4* v_rec;                    // [n_vstrips + 1] (first VN, k, degree, first run)
+  int2* v_runs;                   // (first stored c2v row, staged row | length << 8)
+};
+
 struct ldpc_graph {
   DevGraph d;
   int* dev_block;  // one allocation for every device array
   int max_dv, max_dc, max_items;
   Tiling flood, layer;
+  Strips sflood, slayer;
+  int* strip_block;
   int* tile_block;
   unsigned char* hop_block;  // precomputed two-hop tables (may be null)
 };
@@ -57,6 +70,83 @@ inline int cuda_check(cudaError_t e) {
 bool is_dynamic(int kind) { return kind != KIND_FLOODING && kind != KIND_LAYERED; }
 
 __host__ __device__ inline long long align16(long long x) { return (x + 15) & ~15ll; }
+
+// Strips of one schedule: per level (checks in level order), runs of
+// consecutive checks with the same degree d, k <= kTileEdges / d per strip,
+// rows slot-major (row q*k + c = slot q of check c); c2v rows are stored in
+// that order.  Total-row runs: maximal spans of consecutive staged rows whose
+// VNs are consecutive (one bulk copy each).
+struct HostStrips {
+  std::vector<int> level_sptr, rec, runs, vn, vn_rows, v_rec, v_runs;
+};
+void build_strips(HostStrips& h, const std::vector<int>& lvl_ptr, const std::vector<int>& chk,
+                  const std::vector<int>& cn_ptr, const int* edge_vn, const std::vector<int>& vn_edges, int E) {
+  std::vector<int> pos(E);
+  h.level_sptr.push_back(0);
+  int row = 0;
+  for (size_t L = 0; L + 1 < lvl_ptr.size(); ++L) {
+    int i = lvl_ptr[L];
+    while (i < lvl_ptr[L + 1]) {
+      const int d = cn_ptr[chk[i] + 1] - cn_ptr[chk[i]];
+      const int kmax = std::max(1, kTileEdges / std::max(1, d));
+      int j = i + 1;
+      while (j < lvl_ptr[L + 1] && j - i < kmax && cn_ptr[chk[j] + 1] - cn_ptr[chk[j]] == d) ++j;
+      const int k = j - i;
+      h.rec.insert(h.rec.end(), {row, k, d, (int)h.runs.size() / 2});
+      int prev = -2, open = -1;
+      for (int q = 0; q < d; ++q)
+        for (int c = 0; c < k; ++c) {
+          const int e = cn_ptr[chk[i + c]] + q, r = q * k + c, v = edge_vn[e];
+          pos[e] = row + r;
+          h.vn.push_back(v);
+          if (open >= 0 && v == prev + 1 && (h.runs[open + 1] >> 8) < 255) {
+            h.runs[open + 1] += 1 << 8;
+          } else {
+            open = (int)h.runs.size();
+            h.runs.push_back(v);
+            h.runs.push_back(r | (1 << 8));
+          }
+          prev = v;
+        }
+      row += k * d;
+      i = j;
+    }
+    h.level_sptr.push_back((int)h.rec.size() / 4);
+  }
+  h.rec.insert(h.rec.end(), {row, 0, 0, (int)h.runs.size() / 2});
+  h.vn_rows.resize(E);
+  for (int x = 0; x < E; ++x) h.vn_rows[x] = pos[vn_edges[x]];
+}
+
+// VN strips over the stored c2v order `vn_rows`: k consecutive VNs of equal
+// degree dv (k*dv <= kTileEdges, k <= kVnStripMax), staged rows s*k + v, runs
+// of consecutive stored rows.
+void build_vn_strips(HostStrips& h, const int* vn_ptr, int N) {
+  int n = 0;
+  while (n < N) {
+    const int dv = vn_ptr[n + 1] - vn_ptr[n];
+    const int kmax = std::min(kVnStripMax, std::max(1, kTileEdges / std::max(1, dv)));
+    int j = n + 1;
+    while (j < N && j - n < kmax && vn_ptr[j + 1] - vn_ptr[j] == dv) ++j;
+    const int k = j - n;
+    h.v_rec.insert(h.v_rec.end(), {n, k, dv, (int)h.v_runs.size() / 2});
+    int prev = -2, open = -1;
+    for (int q = 0; q < dv; ++q)
+      for (int v = 0; v < k; ++v) {
+        const int r = q * k + v, row = h.vn_rows[vn_ptr[n + v] + q];
+        if (open >= 0 && row == prev + 1 && (h.v_runs[open + 1] >> 8) < 255) {
+          h.v_runs[open + 1] += 1 << 8;
+        } else {
+          open = (int)h.v_runs.size();
+          h.v_runs.push_back(row);
+          h.v_runs.push_back(r | (1 << 8));
+        }
+        prev = row;
+      }
+    n = j;
+  }
+  h.v_rec.insert(h.v_rec.end(), {N, 0, 0, (int)h.v_runs.size() / 2});
+}
 
 int sm_count() {
   static int n = 0;
@@ -254,7 +344,7 @@ struct FixedPlan {
   long long ws_bytes;
 };
 
-int fixed_engine_choice();
+int fixed_engine_choice(const ldpc_sched_t* s, long long B);
 
 // traced flooding / layered (fixed_trace.cu): one warp per frame, state in HBM
 struct FixedTracePlan {
@@ -285,7 +375,7 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
   const bool layered = s->kind == KIND_LAYERED;
   pl.p.slot_bytes = align16((2ll * G->d.N + G->d.E) * F * sizeof(T) + 4ll * G->d.N);
   pl.threads = 512;
-  const bool pipe = fixed_engine_choice() == 2;
+  const bool pipe = fixed_engine_choice(s, B) == 2;
   pl.smem_bytes = (pipe ? 1 + 2 * kFixedStages : (layered ? 2 : 1)) * kTileEdges * F * (int)sizeof(T);
   if (pl.smem_bytes > smem_optin() - 1024) return LDPC_ERR_UNSUPPORTED;
   void* fn = pipe ? ldpc_fixed_pipe_kernel(sizeof(T) == 8, s->kernel, layered) : pick_fixed_kernel<T>(s->kernel, layered);
@@ -316,12 +406,28 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
 
 // Engine choice for flooding / layered: "phase" (batch-wide phases, default),
 // "tile" (one persistent CTA per 32-frame group), "pipe" (tile + cp.async).
-int fixed_engine_choice() {
+int fixed_engine_choice(const ldpc_sched_t* s, long long B) {
   const char* e = getenv("LDPC_FIXED_ENGINE");
-  if (!e) return 0;
-  if (!strcmp(e, "tile")) return 1;
-  if (!strcmp(e, "pipe")) return 2;
+  if (e) {
+    if (!strcmp(e, "tile")) return 1;
+    if (!strcmp(e, "pipe")) return 2;
+    return 0;
+  }
+  // float64 with many waves of 32-frame groups: the per-group persistent
+  // kernel keeps each group's state L2-hot across iterations and has no tail
+  // to speak of (measured on C1: 1.2-1.8x the phase engine); otherwise phases.
+  const long long groups = (B + kFixedFrames - 1) / kFixedFrames;
+  if (s->precision == LDPC_F64 && groups >= 16ll * sm_count()) return 1;
   return 0;
+}
+
+// Phase engine: the TMA-fed strip kernels (fixed_tma.cuh) except float64
+// flooding, where the load-wait-compute kernel measured faster (C3: 27 vs 40 ms
+// per check launch); LDPC_PHASE_CHECK=legacy|tma overrides.
+bool phase_use_tma(const ldpc_sched_t* s) {
+  const char* pc = getenv("LDPC_PHASE_CHECK");
+  if (pc) return !!strcmp(pc, "legacy");
+  return !(s->precision == LDPC_F64 && s->kind == KIND_FLOODING);
 }
 
 struct PhasePlan {
@@ -353,11 +459,17 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   const bool layered = s->kind == KIND_LAYERED;
   const PhaseKernels K = ldpc_phase_kernels(sizeof(T) == 8, s->kernel, layered);
   const Tiling& tl = layered ? G->layer : G->flood;
-  const std::vector<int>& lvl = tl.h_level_tptr;
+  const Strips& sp = layered ? G->slayer : G->sflood;
   cudaFuncSetAttribute(K.check, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_check);
-  auto grid_of = [&](void* fn, int smem, long long items) {
+  // check phase: the TMA-fed warp-specialised kernel unless LDPC_PHASE_CHECK=legacy
+  const bool use_tma = phase_use_tma(s);
+  if (use_tma) {
+    cudaFuncSetAttribute(K.check_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
+    cudaFuncSetAttribute(K.vn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.vn_smem);
+  }
+  auto grid_of = [&](void* fn, int smem, long long items, int threads = kPhaseThreads) {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPhaseThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) occ = 1;
     return (int)std::max<long long>(1, std::min<long long>((long long)occ * sm_count(), items));
   };
   const int I = s->i_max;
@@ -396,14 +508,22 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.te_chk = tl.te_chk;
     p.tile_cptr = tl.tile_cptr;
     p.tc_rec = tl.tc_rec;
+    p.s_rec = sp.rec;
+    p.s_runs = sp.runs;
+    p.s_vn = sp.vn;
+    p.vn_rows = use_tma ? sp.vn_rows : G->d.vn_edges;  // legacy flooding stores c2v in edge order
+    p.v_rec = sp.v_rec;
+    p.v_runs = sp.v_runs;
+    p.n_vstrips = sp.n_vstrips;
     if (int rc = cuda_check(cudaMemsetAsync(p.errs, 0, 2ll * pl.chunk * kFixedFrames * 4, st))) return rc;
     const long long G_ = p.groups;
     const long long vch = (G->d.N + kPhaseVnChunk - 1) / kPhaseVnChunk;
     const long long ech = ((long long)G->d.E + kPhaseVnChunk * 8 - 1) / (kPhaseVnChunk * 8);
     const long long cch = (G->d.M + kPhaseChkChunk - 1) / kPhaseChkChunk;
-    auto launch = [&](void* fn, long long items, int smem, void** args, int threads = kPhaseThreads) {
+    auto launch = [&](void* fn, long long items, int smem, void** args, int threads = kPhaseThreads,
+                      bool persistent = true) {
       ++launches;
-      const int grid = threads == kPhaseThreads ? grid_of(fn, smem, items) : (int)items;
+      const int grid = persistent ? grid_of(fn, smem, items, threads) : (int)items;
       return cuda_check(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, st));
     };
     void* a1[] = {&p};
@@ -415,19 +535,28 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
       if (int rc = launch(K.syndrome, G_ * cch, 0, a1)) return rc;
     k = 0;
     chk = I == 0 ? 1 : 0;
-    if (int rc = launch(K.finalize, fin_blocks, 0, af, 256)) return rc;
+    if (int rc = launch(K.finalize, fin_blocks, 0, af, 256, false)) return rc;
     for (int it = 1; it <= I; ++it) {
-      for (int L = 0; L < tl.n_levels; ++L) {
+      const std::vector<int>& lvl = use_tma ? sp.h_level_sptr : tl.h_level_tptr;
+      for (int L = 0; L + 1 < (int)lvl.size(); ++L) {
         int t_lo = lvl[L], t_hi = lvl[L + 1];
         if (t_hi <= t_lo) continue;
         void* ac[] = {&p, &t_lo, &t_hi};
-        if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) return rc;
+        if (use_tma) {
+          if (int rc = launch(K.check_tma, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
+        } else if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) {
+          return rc;
+        }
       }
-      if (int rc = launch(K.vn, G_ * vch, 0, a1)) return rc;
+      if (use_tma && !layered) {
+        if (int rc = launch(K.vn_tma, G_ * sp.n_vstrips, K.vn_smem, a1, K.vn_threads)) return rc;
+      } else if (int rc = launch(K.vn, G_ * vch, 0, a1)) {
+        return rc;
+      }
       if (int rc = launch(K.syndrome, G_ * cch, 0, a1)) return rc;
       k = it;
       chk = 1;
-      if (int rc = launch(K.finalize, fin_blocks, 0, af, 256)) return rc;
+      if (int rc = launch(K.finalize, fin_blocks, 0, af, 256, false)) return rc;
     }
     if (int rc = launch(K.output, G_ * vch, 0, a1)) return rc;
   }
@@ -529,7 +658,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
                                              pl.smem_bytes, st)))
       return rc;
     g_last_launches = 1;
-  } else if (fixed_engine_choice() == 0) {
+  } else if (fixed_engine_choice(s, B) == 0) {
     return phase_decode<T>(G, llr, B, s, u_hat, props, conv, counters, biterr, biterr_info, ws, ws_bytes, st);
   } else {
     FixedPlan pl;
@@ -872,10 +1001,58 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     }
     G->tile_block = tb;
   }
+  {  // strips of both schedules: one more device block
+    HostStrips hs[2];
+    std::vector<int> all(M), one = {0, M}, ve(vn_edges, vn_edges + E), cp(cn_ptr, cn_ptr + M + 1);
+    for (int m = 0; m < M; ++m) all[m] = m;
+    build_strips(hs[0], one, all, cp, edge_vn, ve, E);
+    build_strips(hs[1], level_ptr, level_checks, cp, edge_vn, ve, E);
+    build_vn_strips(hs[0], vn_ptr, N);
+    std::vector<int> hb;
+    size_t off[2][6];
+    for (int i = 0; i < 2; ++i) {
+      while (hb.size() % 4) hb.push_back(0);
+      off[i][0] = hb.size();
+      hb.insert(hb.end(), hs[i].rec.begin(), hs[i].rec.end());
+      off[i][1] = hb.size();
+      hb.insert(hb.end(), hs[i].runs.begin(), hs[i].runs.end());
+      off[i][2] = hb.size();
+      hb.insert(hb.end(), hs[i].vn.begin(), hs[i].vn.end());
+      off[i][3] = hb.size();
+      hb.insert(hb.end(), hs[i].vn_rows.begin(), hs[i].vn_rows.end());
+      while (hb.size() % 4) hb.push_back(0);
+      off[i][4] = hb.size();
+      hb.insert(hb.end(), hs[i].v_rec.begin(), hs[i].v_rec.end());
+      off[i][5] = hb.size();
+      hb.insert(hb.end(), hs[i].v_runs.begin(), hs[i].v_runs.end());
+    }
+    int* sb = nullptr;
+    if (cudaMalloc(&sb, hb.size() * sizeof(int)) != cudaSuccess ||
+        cudaMemcpy(sb, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (sb) cudaFree(sb);
+      cudaFree(G->tile_block);
+      cudaFree(d);
+      delete G;
+      return LDPC_ERR_CUDA;
+    }
+    Strips* dst[2] = {&G->sflood, &G->slayer};
+    for (int i = 0; i < 2; ++i) {
+      dst[i]->h_level_sptr = hs[i].level_sptr;
+      dst[i]->rec = (int4*)(sb + off[i][0]);
+      dst[i]->runs = (int2*)(sb + off[i][1]);
+      dst[i]->vn = sb + off[i][2];
+      dst[i]->vn_rows = sb + off[i][3];
+      dst[i]->n_vstrips = hs[i].v_rec.empty() ? 0 : (int)hs[i].v_rec.size() / 4 - 1;
+      dst[i]->v_rec = (int4*)(sb + off[i][4]);
+      dst[i]->v_runs = (int2*)(sb + off[i][5]);
+    }
+    G->strip_block = sb;
+  }
   if (want_tab) {  // two-hop tables: their own allocation
     const size_t bytes = hop_items.size() * 4 + (size_t)E * 8 + (size_t)E * 4 + hop_sb.size() * 4 + 64;
     unsigned char* hb = nullptr;
     if (cudaMalloc(&hb, bytes) != cudaSuccess) {
+      cudaFree(G->strip_block);
       cudaFree(G->tile_block);
       cudaFree(d);
       delete G;
@@ -889,6 +1066,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
               cudaMemcpy(hb + o_sb, hop_sb.data(), hop_sb.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) {
       cudaFree(hb);
+      cudaFree(G->strip_block);
       cudaFree(G->tile_block);
       cudaFree(d);
       delete G;
@@ -934,6 +1112,7 @@ int ldpc_graph_destroy(ldpc_graph_t* G) {
   if (!G) return LDPC_ERR_INVALID;
   cudaFree(G->dev_block);
   cudaFree(G->tile_block);
+  cudaFree(G->strip_block);
   if (G->hop_block) cudaFree(G->hop_block);
   delete G;
   return LDPC_OK;
@@ -966,7 +1145,7 @@ int ldpc_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B,
       int rc = s->precision == LDPC_F64 ? fixed_trace_plan<double>(G, s, B, pl) : fixed_trace_plan<float>(G, s, B, pl);
       if (rc) return rc;
       ws = pl.ws_bytes;
-    } else if (fixed_engine_choice() == 0) {
+    } else if (fixed_engine_choice(s, B) == 0) {
       PhasePlan pl;
       if (s->precision == LDPC_F64) phase_plan<double>(G, B, pl);
       else phase_plan<float>(G, B, pl);

@@ -97,13 +97,23 @@ template <> struct Num<float> {
   static constexpr float kLlrMax = 30.0f;
   static constexpr float kAtanhClip = (float)(1.0 - 1e-12);  // rounds to 1.0f: fp32 saturates earlier
   static constexpr float kBig = 3.0e38f;
-  // fp32 fast mode (no bit-parity obligation; tested statistically): SFU forms
+  // fp32 fast mode (no bit-parity obligation; tested statistically): SFU
+  // forms with flush-to-zero (ex2 / rcp / lg2 approx), and short series where
+  // the SFU forms cancel (small |x|), so relative errors stay ~1e-6.
+  __device__ static float ex2f(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+  __device__ static float rcpf(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+  __device__ static float lg2f(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
   __device__ static float tanh_(float x) {
     const float a = fabsf(x);
-    const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * a) + 1.0f);
-    return copysignf(a < 0.004f ? a : t, x);  // small |x|: tanh x = x to fp32 precision
+    const float t = 1.0f - 2.0f * rcpf(ex2f(2.8853900817779268f * a) + 1.0f);  // 1 - 2/(e^{2a}+1)
+    const float s = a * (1.0f - 0.33333333f * a * a);                             // a - a^3/3
+    return copysignf(a < 0.03f ? s : t, x);
   }
-  __device__ static float atanh_(float x) { return 0.5f * __logf(__fdividef(1.0f + x, 1.0f - x)); }
+  __device__ static float atanh_(float x) {
+    const float l = 0.34657359027997264f * lg2f((1.0f + x) * rcpf(1.0f - x));  // 0.5 ln((1+x)/(1-x))
+    const float s = x * (1.0f + 0.33333333f * x * x);                           // x + x^3/3
+    return fabsf(x) < 0.03f ? s : l;
+  }
   __device__ static float exp_(float x) { return __expf(x); }
   __device__ static float abs_(float x) { return fabsf(x); }
   __device__ static Key key(float v) { return v >= 0.0f ? __float_as_uint(v) + 1u : 0u; }

@@ -186,3 +186,66 @@ def test_device_frame_generation_statistics():
     fd = (dev["bit_errors_at"][:, -1] > 0).mean()
     fh = (host["bit_errors_at"][:, -1] > 0).mean()
     assert abs(fd - fh) < 2.58 * np.sqrt(2 * fh * (1 - fh) / 20000) + 1e-3
+
+
+def _with_env(name, value, fn):
+    import os
+    old = os.environ.get(name)
+    os.environ[name] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[name]
+        else:
+            os.environ[name] = old
+
+
+@pytest.mark.parametrize("code_key,eb,i_max,count", [("C0", 2.0, 5, 700), ("C2", 1.0, 3, 200), ("C3", 1.0, 2, 40)])
+@pytest.mark.parametrize("kernel", ["exact", "minsum"])
+def test_fixed_check_engines_match(code_key, eb, i_max, count, kernel):
+    """TMA-fed strip kernels (fixed_tma.cuh) == the load-wait-compute phase
+    kernels == the per-group persistent kernel, bit for bit in float64,
+    flooding and layered (odd batch: a partial group)."""
+    spec, g = load_code(code_key)
+    llrs = llr_batch(spec, eb, seed=5, start=0, count=count)
+    for kind in ("flooding", "layered"):
+        cfg = _cfg({"kind": kind, "i_max": i_max, "kernel": kernel})
+        a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
+        b = _with_env("LDPC_PHASE_CHECK", "legacy", lambda: _gpu(spec, llrs, cfg))
+        c = _with_env("LDPC_FIXED_ENGINE", "tile", lambda: _gpu(spec, llrs, cfg))
+        for k in FIELDS:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=f"{code_key} {kind} {kernel} {k}")
+            np.testing.assert_array_equal(a[k], c[k], err_msg=f"{code_key} {kind} {kernel} {k} (tile engine)")
+
+
+@pytest.mark.parametrize("kind", ["flooding", "layered"])
+def test_fixed_high_degree_checks_vs_oracle(kind):
+    """Check degree 20 (> the unrolled degrees): the generic output path."""
+    from paper_2102_11089_b200.codes import build_tanner, make_random_regular_code
+    spec = make_random_regular_code(400, 2, 20, seed=1)
+    g = build_tanner(spec.h)
+    llrs = llr_batch(spec, 4.0, seed=2, start=0, count=300)
+    for kernel in ("exact", "minsum"):
+        _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 4, "kernel": kernel}), min_frac=1.0)
+
+
+@pytest.mark.parametrize("kind", ["flooding", "layered"])
+def test_fixed_fp32_statistics(kind):
+    """fp32 fixed schedules (SFU math, FMA): FER within noise of float64 and
+    almost all frames decided identically (C0), and BG1-shaped bit-error
+    counts within a few percent."""
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=0, start=0, count=4000)
+    a = _gpu(spec, llrs, _cfg({"kind": kind, "i_max": 5}))
+    b = _gpu(spec, llrs, _cfg({"kind": kind, "i_max": 5, "precision": "f32"}))
+    fa = (a["bit_errors_at"][:, -1] > 0).mean()
+    fb = (b["bit_errors_at"][:, -1] > 0).mean()
+    assert abs(fa - fb) < 4 * np.sqrt(fa * (1 - fa) / len(llrs)) + 1e-3
+    assert ((a["u_hat"] == b["u_hat"]).all(1)).mean() > 0.97
+    spec3, _ = load_code("C3")
+    l3 = llr_batch(spec3, 1.0, seed=0, start=0, count=32)
+    c = _gpu(spec3, l3, _cfg({"kind": kind, "i_max": 3}))
+    d = _gpu(spec3, l3, _cfg({"kind": kind, "i_max": 3, "precision": "f32"}))
+    ea, eb_ = c["bit_errors_at"][:, -1].sum(), d["bit_errors_at"][:, -1].sum()
+    assert abs(int(ea) - int(eb_)) <= 0.02 * ea + 10
