@@ -74,12 +74,14 @@ __device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned t
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase completes
+// (or the hint expires) instead of spinning on issue slots
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
   unsigned ok;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
@@ -113,6 +115,15 @@ __device__ __forceinline__ void strip_commit(const T* so, const T* st, const int
   c2v[(e0 + r) * F + lane] = out;
   if (LAYERED) total[(long long)tv[r] * F + lane] = st[r * F + lane] + (out - so[r * F + lane]);
 }
+// same, with the check's row pointers precomputed (row r = q*k + c):
+// cq = c2v row of slot 0 + q*k*F, xq = staged offset
+template <typename T, bool LAYERED>
+__device__ __forceinline__ void strip_commit_p(const T* so, const T* st, const int* tv, int r, int xq, T* cq, T out,
+                                               T* total, int lane) {
+  constexpr int F = kFixedFrames;
+  *cq = out;
+  if (LAYERED) total[(long long)tv[r] * F + lane] = st[xq] + (out - so[xq]);
+}
 
 // All outputs of check c of a strip (k checks of degree D, slot-major rows).
 // float64 keeps the reference's left-to-right product (shared prefix, then
@@ -122,9 +133,11 @@ template <typename T, int KERNEL, bool LAYERED, int D>
 __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const int* tv, int c, int k, long long e0,
                                               int lane, T* c2v, T* total) {
   constexpr int F = kFixedFrames;
+  const int x0 = c * F + lane, xs = k * F;     // staged offset of slot 0, slot stride
+  T* c0 = c2v + ((e0 + c) * F + lane);         // stored c2v row of slot 0
   T in[D];
 #pragma unroll
-  for (int q = 0; q < D; ++q) in[q] = staged_in<T, KERNEL>(so, st, (q * k + c) * F + lane);
+  for (int q = 0; q < D; ++q) in[q] = staged_in<T, KERNEL>(so, st, x0 + q * xs);
   if (KERNEL == KERNEL_EXACT) {
     constexpr bool kSuffix = sizeof(T) == 4;
     T suf[D];
@@ -147,7 +160,7 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
         for (int r = q + 1; r < D; ++r) prod *= in[r];
       }
       pre *= in[q];
-      strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, atanh_msg(prod, D - 1), c2v, total);
+      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, atanh_msg(prod, D - 1), total, lane);
     }
   } else {
     T m1 = Num<T>::kBig, m2 = Num<T>::kBig, sgn = T(1);
@@ -173,7 +186,7 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
     for (int q = 0; q < D; ++q) {
       const T sign = ((negs >> q) & 1u) ? -sgn : sgn;
       const T out = D > 1 ? clampv(sign * (q == i1 ? m2 : m1)) : T(0);
-      strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, out, c2v, total);
+      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, out, total, lane);
     }
   }
 }
@@ -250,12 +263,12 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
   }
   __syncthreads();
   const int nti = t_hi - t_lo;
-  const long long items = (long long)p.groups * nti;
+  const long long items = (long long)p.groups * nti;  // < 2^31 (groups * strips); divisions in 32 bits
 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x)
-        if (p.amask[i / nti]) break;
+        if (p.amask[(unsigned)i / (unsigned)nti]) break;
       return i;
     };
     long long it = seek(blockIdx.x);
@@ -265,7 +278,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     int vn[RPL];
     auto prefetch = [&](long long i) {
       if (i >= items) return;
-      const int t = t_lo + (int)(i % nti);
+      const int t = t_lo + (int)((unsigned)i % (unsigned)nti);
       rec = p.s_rec[t];
       nrun = p.s_rec[t + 1].w - rec.w;
 #pragma unroll
@@ -280,7 +293,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
-      GroupSlot<T> gs(p, it / nti);
+      GroupSlot<T> gs(p, (unsigned)it / (unsigned)nti);
       const int rows = rec.y * rec.z;
       if (LAYERED) {
         int* tv = tv_of(s);
@@ -308,13 +321,13 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
   } else {  // ---------------- consumers
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
-      const long long grp = it / nti;
+      const int grp = (int)((unsigned)it / (unsigned)nti);
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.s_rec[t_lo + (int)(it - grp * nti)];
+      const int4 rec = p.s_rec[t_lo + (int)(it - (long long)grp * nti)];
       GroupSlot<T> gs(p, grp);
       mbar_wait(&full[s], u & 1u);
       if ((am >> lane) & 1u)
@@ -354,7 +367,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x)
-        if (p.amask[i / nvs]) break;
+        if (p.amask[(unsigned)i / (unsigned)nvs]) break;
       return i;
     };
     long long it = seek(blockIdx.x);
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
     int2 run[RPL];
     auto prefetch = [&](long long i) {
       if (i >= items) return;
-      const int t = (int)(i % nvs);
+      const int t = (int)((unsigned)i % (unsigned)nvs);
       rec = p.v_rec[t];
       nrun = p.v_rec[t + 1].w - rec.w;
 #pragma unroll
@@ -375,7 +388,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
-      GroupSlot<T> gs(p, it / nvs);
+      GroupSlot<T> gs(p, (unsigned)it / (unsigned)nvs);
       const int k = rec.y, erows = k * rec.z;
       T* sb = stage(s);
       if (lane == 0) {
@@ -396,13 +409,13 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
   } else {  // ---------------- consumers
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
-      const long long grp = it / nvs;
+      const int grp = (int)((unsigned)it / (unsigned)nvs);
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.v_rec[(int)(it - grp * nvs)];
+      const int4 rec = p.v_rec[(int)(it - (long long)grp * nvs)];
       GroupSlot<T> gs(p, grp);
       const bool act = (am >> lane) & 1u;
       const int k = rec.y, dv = rec.z;

@@ -35,6 +35,7 @@ struct Strips {  // slot-major check strips of the TMA-fed check phase (fixed_tm
   int2* runs;                     // (first VN, staged row | length << 8)
   int* vn;                        // [E] VN of each staged / stored row
   int* vn_rows;                   // [E] stored c2v row of each vn_edges slot
+  int rec_count;                  // number of check strips
   int n_vstrips;                  // VN strips (flooding VN phase)
   int4* v_rec;                    // [n_vstrips + 1] (first VN, k, degree, first run)
   int2* v_runs;                   // (first stored c2v row, staged row | length << 8)
@@ -443,6 +444,10 @@ int phase_plan(const ldpc_graph* G, long long B, PhasePlan& pl) {
   pl.groups = (B + F - 1) / F;
   const long long per_group_state = 4 + 4 + 3 * 4 * F;  // amask, unsat, errs, errs_info, iters
   pl.chunk = std::max<long long>(1, std::min(pl.groups, (24ll << 30) / (pl.slot + per_group_state)));
+  // the strip kernels index (group, strip) items in 32 bits
+  const long long strips = std::max<long long>({1, (long long)G->sflood.rec_count, (long long)G->slayer.rec_count,
+                                                (long long)G->sflood.n_vstrips});
+  pl.chunk = std::min(pl.chunk, std::max<long long>(1, 0x7fffffffll / strips));
   pl.state_off = 256 + pl.chunk * pl.slot;
   pl.ws_bytes = pl.state_off + align16(pl.chunk * per_group_state) + 64;
   pl.smem_check = 3 * kTileEdges * (int)F * (int)sizeof(T);
@@ -1043,6 +1048,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       dst[i]->vn = sb + off[i][2];
       dst[i]->vn_rows = sb + off[i][3];
       dst[i]->n_vstrips = hs[i].v_rec.empty() ? 0 : (int)hs[i].v_rec.size() / 4 - 1;
+      dst[i]->rec_count = (int)hs[i].rec.size() / 4 - 1;
       dst[i]->v_rec = (int4*)(sb + off[i][4]);
       dst[i]->v_runs = (int2*)(sb + off[i][5]);
     }

@@ -142,6 +142,15 @@ template <typename T> __device__ __forceinline__ T atanh_msg(T prod, int count) 
   else if (prod < -Num<T>::kAtanhClip) prod = -Num<T>::kAtanhClip;
   return clampv(T(2) * Num<T>::atanh_(prod));
 }
+// fp32: the clip point rounds to 1.0f, where ln((1+x)/(1-x)) is +-inf and the
+// +-30 clamp applies anyway (x = -1 gives lg2(0) = -inf), so no clip is needed;
+// 2 atanh(x) = ln2 * lg2((1+x)/(1-x)), or 2x + 2x^3/3 for small |x|.
+template <> __device__ __forceinline__ float atanh_msg<float>(float x, int count) {
+  if (count == 0) return 0.0f;
+  const float l = 0.69314718055994531f * Num<float>::lg2f((1.0f + x) * Num<float>::rcpf(1.0f - x));
+  const float s = x * (2.0f + 0.66666667f * x * x);
+  return clampv(fabsf(x) < 0.03f ? s : l);
+}
 
 // C2V of check [a, b) excluding edge `skip` from cached inputs `in`:
 // exact kernel: in = tanh(v2c/2) (E:85-103); min-sum: in = v2c (E:67-82).
