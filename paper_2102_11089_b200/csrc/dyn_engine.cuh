@@ -39,6 +39,13 @@ namespace ldpc {
 #ifndef LDPC_DYN_MIN_BLOCKS
 #define LDPC_DYN_MIN_BLOCKS 4
 #endif
+// Resident 256-thread blocks per SM the register budget is cut for: 4 (64
+// registers) in general; the float64 RBP and LMDRBP kernels run faster at 6
+// (40 registers, more spills, 1.5x the resident frames: C1 -3 % / -16 %),
+// while the CI and ME kinds lose (measured with tools/dyn_sweep.py).
+constexpr int dyn_min_blocks(int kind, bool f64) {
+  return (f64 && (kind == KIND_RBP || kind == KIND_LMDRBP)) ? 6 : LDPC_DYN_MIN_BLOCKS;
+}
 
 constexpr int kFlatCiMax = 128;  // CIRBP: flat CI argmax when N <= this (else incremental tree)
 
@@ -1354,7 +1361,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
 // 2: E and N in HBM, T in shared; 3: everything in HBM.  G lanes per frame
 // (32/G frames per warp); slots and scratch are per frame.
 template <typename T, int KERNEL, int MODE, int KF, int G, bool TR = false>
-__global__ void __launch_bounds__(256, LDPC_DYN_MIN_BLOCKS) dyn_decode_kernel(const __grid_constant__ DynParams p) {
+__global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int FPW = 32 / G;  // frames per warp
   const int fpb = (blockDim.x >> 5) * FPW;

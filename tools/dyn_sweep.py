@@ -1,11 +1,12 @@
 """Resident-frame / placement sweep for the dynamic engine (sets the dyn_plan policy).
 
-    python tools/dyn_sweep.py CODE KINDS [B] [f64|f32]
+    python tools/dyn_sweep.py CODE KINDS [B] [f64|f32] [placements] [fractions]
 KINDS: comma list, ME kinds as me_cirbp/4.  For each kind, placement in
 auto/split/trees/hbm and max_resident in {auto, 1/4, 1/2, 3/4 of auto}:
 one JSON line with ms and updates/s.
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -22,6 +23,8 @@ key = sys.argv[1]
 kinds = sys.argv[2].split(",")
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 100_000
 prec = sys.argv[4] if len(sys.argv) > 4 else "f64"
+PLACES = sys.argv[5].split(",") if len(sys.argv) > 5 else ["auto", "split", "trees", "hbm"]
+FRACS = [float(x) for x in sys.argv[6].split(",")] if len(sys.argv) > 6 else [0, 0.25, 0.5, 0.75]
 eb, imax = EB[key]
 spec = getattr(configs, f"make_{'c2' if key == 'C4' else key.lower()}_code")()
 g = build_tanner(spec.h)
@@ -43,8 +46,8 @@ def timed(cfg, **kw):
 for ks in kinds:
     kind, _, m = ks.partition("/")
     cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=int(m or 1), precision=prec)
-    for pl in ("auto", "split", "trees", "hbm"):
-        for frac in (0, 0.25, 0.5, 0.75):
+    for pl in PLACES:
+        for frac in FRACS:
             res = 0
             if frac:
                 res = max(32, int(frac * min(B, 148 * 64)))
@@ -53,5 +56,5 @@ for ks in kinds:
             except Exception as e:  # unsupported placement for this kind/code
                 print(json.dumps({"kind": ks, "placement": pl, "res": res, "error": str(e)[:80]}), flush=True)
                 break
-            print(json.dumps({"code": key, "kind": ks, "placement": pl, "res": res, "ms": round(ms, 2),
+            print(json.dumps({"lib": os.environ.get("LDPC_B200_LIB", "default")[-12:], "code": key, "kind": ks, "placement": pl, "res": res, "ms": round(ms, 2),
                               "upd_per_s": upd / ms * 1e3}), flush=True)
