@@ -64,6 +64,8 @@ struct PhaseParams {
   const int4* v_rec;
   const int2* v_runs;
   int n_vstrips;
+  const int* s_lvl;  // [levels + 1] first strip of each level (check strips)
+  int* done;         // [groups] committed check strips per group (layered, levels fused in one launch)
 };
 
 #ifndef LDPC_PHASE_DECL_ONLY  // the host launcher only needs PhaseParams

@@ -85,6 +85,16 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
       : "memory");
   return ok != 0;
 }
+// non-blocking probe of a phase
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   while (!mbar_try(b, parity)) {
   }
@@ -240,11 +250,49 @@ __device__ __forceinline__ void strip_checks(const T* so, const T* st, const int
 
 #ifndef LDPC_PHASE_DECL_ONLY
 
-// Check phase over the strips [t_lo, t_hi) of one level, all active groups.
+// (group, strip) items of the levels [L0, L1): level-major, then group, then
+// strip, so a level's items of one group are contiguous and every item's
+// dependencies (the group's earlier levels) come earlier in the order.
+struct LevelMap {
+  const int* lp;  // strip prefix per level (lp[L] = first strip of level L)
+  int L, L1, G, P, nL;
+  long long lo, hi;  // item range of level L
+  __device__ LevelMap(const int* lp_, int L0, int L1_, int G_) : lp(lp_), L(L0), L1(L1_), G(G_) {
+    lo = 0;
+    P = lp[L];
+    nL = lp[L + 1] - P;
+    hi = (long long)G * nL;
+  }
+  __device__ __forceinline__ void seek(long long i) {
+    while (i >= hi && L + 1 < L1) {
+      ++L;
+      lo = hi;
+      P = lp[L];
+      nL = lp[L + 1] - P;
+      hi = lo + (long long)G * nL;
+    }
+  }
+  __device__ __forceinline__ int group(long long i) const { return (int)((unsigned)(i - lo) / (unsigned)nL); }
+  __device__ __forceinline__ int strip(long long i, int g) const { return P + (int)(i - lo - (long long)g * nL); }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// Check phase over the strips of levels [L0, L1), all active groups.
 // Block = NC consumer warps + 1 producer warp (the last one).
+// dep_base >= 0 (layered, all levels in one launch): an item of level L of
+// group g starts loading totals only once p.done[g] >= dep_base + lp[L], i.e.
+// once every strip of the group's earlier levels of this iteration has been
+// committed (one release-increment per finished item) -- the level order of
+// the reference sweep is kept per group while different groups run different
+// levels, with no grid-wide barrier or relaunch between levels.
 template <typename T, int KERNEL, bool LAYERED, int NC>
 __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::kMinBlocks)
-    phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int t_lo, int t_hi) {
+    phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int L0, int L1, int dep_base) {
   using L = TmaLayout<T, NC>;
   constexpr int F = kFixedFrames, S = kTmaStages, RPL = kTileEdges / 32;  // runs / rows per lane
   extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -262,23 +310,27 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     mbar_fence_init();
   }
   __syncthreads();
-  const int nti = t_hi - t_lo;
-  const long long items = (long long)p.groups * nti;  // < 2^31 (groups * strips); divisions in 32 bits
+  const long long items = (long long)p.groups * (p.s_lvl[L1] - p.s_lvl[L0]);  // < 2^31
+  LevelMap lm(p.s_lvl, L0, L1, p.groups);
 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
-      for (; i < items; i += gridDim.x)
-        if (p.amask[(unsigned)i / (unsigned)nti]) break;
+      for (; i < items; i += gridDim.x) {
+        lm.seek(i);
+        if (p.amask[lm.group(i)]) break;
+      }
       return i;
     };
     long long it = seek(blockIdx.x);
     int4 rec = make_int4(0, 0, 0, 0);
-    int nrun = 0;
+    int nrun = 0, grp = 0, need = 0;
     int2 run[RPL];
     int vn[RPL];
     auto prefetch = [&](long long i) {
       if (i >= items) return;
-      const int t = t_lo + (int)((unsigned)i % (unsigned)nti);
+      grp = lm.group(i);
+      const int t = lm.strip(i, grp);
+      need = dep_base + lm.P;
       rec = p.s_rec[t];
       nrun = p.s_rec[t + 1].w - rec.w;
 #pragma unroll
@@ -289,17 +341,48 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
       }
     };
     prefetch(it);
-    for (int kk = 0; it < items; ++kk) {
+    // Publication of finished items (levels fused): the consumers' stores are
+    // released to this warp by their "empty" arrivals; a gpu-scope fence then
+    // makes them visible before the group's counter moves.  Items are
+    // published in issue order (pub_k = oldest unpublished), eagerly while
+    // this warp waits on a dependency, so a waiting CTA never holds back a
+    // finished item another CTA depends on.
+    int pub[S];
+    int pub_k = 0, kk = 0;
+    auto publish_upto = [&](int k_end, bool block) {  // items [pub_k, k_end)
+      while (pub_k < k_end) {
+        const int s = pub_k % S;
+        const unsigned par = (unsigned)(pub_k / S) & 1u;
+        if (block) mbar_wait(&empty[s], par);
+        else if (!mbar_test(&empty[s], par)) return;
+        if (dep_base >= 0 && lane == 0) {
+          int g = 0;
+#pragma unroll
+          for (int q = 0; q < S; ++q)
+            if (q == s) g = pub[q];
+          __threadfence();
+          atomicAdd(p.done + g, 1);
+        }
+        ++pub_k;
+      }
+    };
+    for (; it < items; ++kk) {
       const int s = kk % S;
-      const unsigned u = (unsigned)(kk / S);
-      if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
-      GroupSlot<T> gs(p, (unsigned)it / (unsigned)nti);
+      if (kk >= S) publish_upto(kk - S + 1, true);  // stage s is free (and its item published)
+      GroupSlot<T> gs(p, grp);
       const int rows = rec.y * rec.z;
       if (LAYERED) {
         int* tv = tv_of(s);
 #pragma unroll
         for (int j = 0; j < RPL; ++j)
           if (lane + 32 * j < rows) tv[lane + 32 * j] = vn[j];
+      }
+      if (dep_base >= 0) {  // the group's earlier levels must be committed
+        while (ld_acquire(p.done + grp) < need) {
+          publish_upto(kk, false);
+          __nanosleep(32);
+        }
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic writes -> TMA reads
       }
       __syncwarp();
       if (lane == 0) {
@@ -315,19 +398,24 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
           bulk_g2s(st + row * F, gs.total + (long long)run[j].x * F, len * L::kRowBytes, &full[s]);
         }
       }
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        if (q == s) pub[q] = grp;
       it = seek(it + gridDim.x);
       prefetch(it);
     }
+    if (dep_base >= 0) publish_upto(kk, true);  // drain: the items still in flight
   } else {  // ---------------- consumers
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
-      const int grp = (int)((unsigned)it / (unsigned)nti);
+      lm.seek(it);
+      const int grp = lm.group(it);
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.s_rec[t_lo + (int)(it - (long long)grp * nti)];
+      const int4 rec = p.s_rec[lm.strip(it, grp)];
       GroupSlot<T> gs(p, grp);
       mbar_wait(&full[s], u & 1u);
       if ((am >> lane) & 1u)
@@ -338,7 +426,6 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     }
   }
 }
-
 
 // VN phase of flooding over VN strips (E:746-756): total = chl + the C2V of
 // the VN's edges in vn_edges order (the reference's summation order), sign

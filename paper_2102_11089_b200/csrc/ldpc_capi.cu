@@ -31,6 +31,7 @@ struct Tiling {  // fixed-engine schedule tiling (see fixed_engine.cuh)
 
 struct Strips {  // slot-major check strips of the TMA-fed check phase (fixed_tma.cuh)
   std::vector<int> h_level_sptr;  // strip range of each level (host copy)
+  int* lvl_sptr;                  // device copy
   int4* rec;                      // [n_strips + 1] (first c2v row, k, d, first run); sentinel .x/.w = totals
   int2* runs;                     // (first VN, staged row | length << 8)
   int* vn;                        // [E] VN of each staged / stored row
@@ -442,7 +443,7 @@ int phase_plan(const ldpc_graph* G, long long B, PhasePlan& pl) {
   pl.sign_off = align16((2 * N + E) * F * (long long)sizeof(T));
   pl.slot = align16(pl.sign_off + 4 * N);
   pl.groups = (B + F - 1) / F;
-  const long long per_group_state = 4 + 4 + 3 * 4 * F;  // amask, unsat, errs, errs_info, iters
+  const long long per_group_state = 4 + 4 + 3 * 4 * F + 4;  // amask, unsat, errs, errs_info, iters, done
   pl.chunk = std::max<long long>(1, std::min(pl.groups, (24ll << 30) / (pl.slot + per_group_state)));
   // the strip kernels index (group, strip) items in 32 bits
   const long long strips = std::max<long long>({1, (long long)G->sflood.rec_count, (long long)G->slayer.rec_count,
@@ -468,6 +469,11 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   cudaFuncSetAttribute(K.check, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_check);
   // check phase: the TMA-fed warp-specialised kernel unless LDPC_PHASE_CHECK=legacy
   const bool use_tma = phase_use_tma(s);
+  // layered: LDPC_LAYERED_FUSE=1 runs all levels in one check launch ordered by
+  // per-group dependency counters; measured equal to one launch per level on
+  // C2/C3 (the check kernel, not the relaunches, bounds the sweep), so off by default
+  const char* fz = getenv("LDPC_LAYERED_FUSE");
+  const bool fuse_levels = fz && !strcmp(fz, "1");
   if (use_tma) {
     cudaFuncSetAttribute(K.check_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
     cudaFuncSetAttribute(K.vn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.vn_smem);
@@ -506,6 +512,8 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.errs = (int*)(p.unsat + pl.chunk);
     p.errs_info = p.errs + pl.chunk * kFixedFrames;
     p.iters = p.errs_info + pl.chunk * kFixedFrames;
+    p.done = p.iters + pl.chunk * kFixedFrames;
+    p.s_lvl = sp.lvl_sptr;
     p.level_tptr = tl.level_tptr;
     p.tile_eptr = tl.tile_eptr;
     p.te_list = tl.te_list;
@@ -521,6 +529,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.v_runs = sp.v_runs;
     p.n_vstrips = sp.n_vstrips;
     if (int rc = cuda_check(cudaMemsetAsync(p.errs, 0, 2ll * pl.chunk * kFixedFrames * 4, st))) return rc;
+    if (int rc = cuda_check(cudaMemsetAsync(p.done, 0, pl.chunk * 4, st))) return rc;
     const long long G_ = p.groups;
     const long long vch = (G->d.N + kPhaseVnChunk - 1) / kPhaseVnChunk;
     const long long ech = ((long long)G->d.E + kPhaseVnChunk * 8 - 1) / (kPhaseVnChunk * 8);
@@ -543,14 +552,24 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     if (int rc = launch(K.finalize, fin_blocks, 0, af, 256, false)) return rc;
     for (int it = 1; it <= I; ++it) {
       const std::vector<int>& lvl = use_tma ? sp.h_level_sptr : tl.h_level_tptr;
-      for (int L = 0; L + 1 < (int)lvl.size(); ++L) {
-        int t_lo = lvl[L], t_hi = lvl[L + 1];
-        if (t_hi <= t_lo) continue;
-        void* ac[] = {&p, &t_lo, &t_hi};
-        if (use_tma) {
-          if (int rc = launch(K.check_tma, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
-        } else if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) {
-          return rc;
+      const int nlev = (int)lvl.size() - 1;
+      if (use_tma && fuse_levels && nlev > 1) {
+        // all levels in one launch; per-group dependency counters keep the order
+        int L0 = 0, L1 = nlev, dep = (it - 1) * lvl[nlev];
+        void* ac[] = {&p, &L0, &L1, &dep};
+        if (int rc = launch(K.check_tma, G_ * lvl[nlev], K.tma_smem, ac, K.tma_threads)) return rc;
+      } else {
+        for (int L = 0; L < nlev; ++L) {
+          int t_lo = lvl[L], t_hi = lvl[L + 1];
+          if (t_hi <= t_lo) continue;
+          if (use_tma) {
+            int L0 = L, L1 = L + 1, dep = -1;
+            void* ac[] = {&p, &L0, &L1, &dep};
+            if (int rc = launch(K.check_tma, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
+          } else {
+            void* ac[] = {&p, &t_lo, &t_hi};
+            if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) return rc;
+          }
         }
       }
       if (use_tma && !layered) {
@@ -1014,7 +1033,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     build_strips(hs[1], level_ptr, level_checks, cp, edge_vn, ve, E);
     build_vn_strips(hs[0], vn_ptr, N);
     std::vector<int> hb;
-    size_t off[2][6];
+    size_t off[2][7];
     for (int i = 0; i < 2; ++i) {
       while (hb.size() % 4) hb.push_back(0);
       off[i][0] = hb.size();
@@ -1030,6 +1049,8 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       hb.insert(hb.end(), hs[i].v_rec.begin(), hs[i].v_rec.end());
       off[i][5] = hb.size();
       hb.insert(hb.end(), hs[i].v_runs.begin(), hs[i].v_runs.end());
+      off[i][6] = hb.size();
+      hb.insert(hb.end(), hs[i].level_sptr.begin(), hs[i].level_sptr.end());
     }
     int* sb = nullptr;
     if (cudaMalloc(&sb, hb.size() * sizeof(int)) != cudaSuccess ||
@@ -1049,6 +1070,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       dst[i]->vn_rows = sb + off[i][3];
       dst[i]->n_vstrips = hs[i].v_rec.empty() ? 0 : (int)hs[i].v_rec.size() / 4 - 1;
       dst[i]->rec_count = (int)hs[i].rec.size() / 4 - 1;
+      dst[i]->lvl_sptr = sb + off[i][6];
       dst[i]->v_rec = (int4*)(sb + off[i][4]);
       dst[i]->v_runs = (int2*)(sb + off[i][5]);
     }

@@ -204,9 +204,10 @@ def _with_env(name, value, fn):
 @pytest.mark.parametrize("code_key,eb,i_max,count", [("C0", 2.0, 5, 700), ("C2", 1.0, 3, 200), ("C3", 1.0, 2, 40)])
 @pytest.mark.parametrize("kernel", ["exact", "minsum"])
 def test_fixed_check_engines_match(code_key, eb, i_max, count, kernel):
-    """TMA-fed strip kernels (fixed_tma.cuh) == the load-wait-compute phase
-    kernels == the per-group persistent kernel, bit for bit in float64,
-    flooding and layered (odd batch: a partial group)."""
+    """TMA-fed strip kernels (fixed_tma.cuh; layered: one launch per level, and
+    all levels in one launch ordered by per-group dependency counters) == the
+    load-wait-compute phase kernels == the per-group persistent kernel, bit for
+    bit in float64, flooding and layered (odd batch: a partial group)."""
     spec, g = load_code(code_key)
     llrs = llr_batch(spec, eb, seed=5, start=0, count=count)
     for kind in ("flooding", "layered"):
@@ -214,9 +215,11 @@ def test_fixed_check_engines_match(code_key, eb, i_max, count, kernel):
         a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
         b = _with_env("LDPC_PHASE_CHECK", "legacy", lambda: _gpu(spec, llrs, cfg))
         c = _with_env("LDPC_FIXED_ENGINE", "tile", lambda: _gpu(spec, llrs, cfg))
+        d = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
         for k in FIELDS:
             np.testing.assert_array_equal(a[k], b[k], err_msg=f"{code_key} {kind} {kernel} {k}")
             np.testing.assert_array_equal(a[k], c[k], err_msg=f"{code_key} {kind} {kernel} {k} (tile engine)")
+            np.testing.assert_array_equal(a[k], d[k], err_msg=f"{code_key} {kind} {kernel} {k} (levels fused)")
 
 
 @pytest.mark.parametrize("kind", ["flooding", "layered"])
@@ -249,3 +252,17 @@ def test_fixed_fp32_statistics(kind):
     d = _gpu(spec3, l3, _cfg({"kind": kind, "i_max": 3, "precision": "f32"}))
     ea, eb_ = c["bit_errors_at"][:, -1].sum(), d["bit_errors_at"][:, -1].sum()
     assert abs(int(ea) - int(eb_)) <= 0.02 * ea + 10
+
+
+@pytest.mark.parametrize("count", [1, 33])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_layered_fused_levels_small_batches(count, precision):
+    """One or two 32-frame groups: every level's items depend on the items just
+    before them (the case the dependency counters must not deadlock on)."""
+    spec, g = load_code("C2")
+    llrs = llr_batch(spec, 1.0, seed=9, start=0, count=count)
+    cfg = _cfg({"kind": "layered", "i_max": 4, "precision": precision})
+    a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
+    b = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
+    for k in FIELDS:
+        np.testing.assert_array_equal(a[k], b[k])

@@ -16,4 +16,4 @@ ncu --set full --clock-control none --import-source on -k regex:phase_check_tma 
 ncu --set full --clock-control none --import-source on -k regex:phase_vn_tma -s 2 -c 1 \
     -o $OUT/prof_c3f_vn_$TAG python bench.py --workload C3F --precision f32 --only flooding --steps 1 --warmup 1 \
     --no-cpu-baseline > $OUT/c3f_ncu_vn.log 2>&1
-tail -1 $OUT/c3f_ncu_full.log $OUT/c3f_ncu_vn.log
+tail -n 1 $OUT/c3f_ncu_full.log; tail -n 1 $OUT/c3f_ncu_vn.log
