@@ -108,6 +108,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 // ------------------------------------------------------ fused check math
+// Layered: the sign-word / error-tally pass (E:192-201) folded into the check
+// phase.  The staged row of a VN's last level in the sweep carries bit 31 in
+// s_vn; its new total is final for the iteration, so the warp ballots the 32
+// frames' signs there (frames already retired contribute their unchanged
+// total) and tallies the bit errors of the active frames.
+struct SignSink {
+  unsigned* sign;
+  int k_info;
+  bool on;
+  int errs, ei;
+};
 // Input of staged row x: tanh(clamp(total - c2v)/2) (E:58) or the clamped V2C
 // (min-sum, E:73).
 template <typename T, int KERNEL>
@@ -118,21 +129,30 @@ __device__ __forceinline__ T staged_in(const T* so, const T* st, int x) {
 
 // Output of staged row r (lane = frame): c2v row e0 + r; layered also commits
 // total[vn] = total_old + (c2v_new - c2v_old).
-template <typename T, bool LAYERED>
-__device__ __forceinline__ void strip_commit(const T* so, const T* st, const int* tv, int r, long long e0, int lane,
-                                             T out, T* c2v, T* total) {
-  constexpr int F = kFixedFrames;
-  c2v[(e0 + r) * F + lane] = out;
-  if (LAYERED) total[(long long)tv[r] * F + lane] = st[r * F + lane] + (out - so[r * F + lane]);
-}
-// same, with the check's row pointers precomputed (row r = q*k + c):
-// cq = c2v row of slot 0 + q*k*F, xq = staged offset
+// Commit of staged row r (offset xq; cq = its stored c2v row): the C2V output,
+// and for layered total[vn] = total_old + (c2v_new - c2v_old) plus, at the
+// VN's last level, its sign word and error tallies.  Stores only for active
+// frames (`act`); the whole warp runs this (the ballot needs every lane).
 template <typename T, bool LAYERED>
 __device__ __forceinline__ void strip_commit_p(const T* so, const T* st, const int* tv, int r, int xq, T* cq, T out,
-                                               T* total, int lane) {
+                                               T* total, int lane, bool act, SignSink& sk) {
   constexpr int F = kFixedFrames;
-  *cq = out;
-  if (LAYERED) total[(long long)tv[r] * F + lane] = st[xq] + (out - so[xq]);
+  if (act) *cq = out;
+  if (LAYERED) {
+    const T nt = st[xq] + (out - so[xq]);
+    const int tvr = tv[r], vn = tvr & 0x7fffffff;
+    if (act) total[(long long)vn * F + lane] = nt;
+    if (sk.on && tvr < 0) {  // warp-uniform: the same staged row in every lane
+      const T fin = act ? nt : st[xq];
+      const bool neg = fin < T(0);
+      const unsigned wsg = __ballot_sync(kFull, neg);
+      if (lane == 0) sk.sign[vn] = wsg;
+      if (act && neg) {
+        ++sk.errs;
+        if (vn < sk.k_info) ++sk.ei;
+      }
+    }
+  }
 }
 
 // All outputs of check c of a strip (k checks of degree D, slot-major rows).
@@ -141,7 +161,7 @@ __device__ __forceinline__ void strip_commit_p(const T* so, const T* st, const i
 // min1 / min2 / sign parity (order-free, same values as E:67-82).
 template <typename T, int KERNEL, bool LAYERED, int D>
 __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const int* tv, int c, int k, long long e0,
-                                              int lane, T* c2v, T* total) {
+                                              int lane, T* c2v, T* total, bool act, SignSink& sk) {
   constexpr int F = kFixedFrames;
   const int x0 = c * F + lane, xs = k * F;     // staged offset of slot 0, slot stride
   T* c0 = c2v + ((e0 + c) * F + lane);         // stored c2v row of slot 0
@@ -170,7 +190,8 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
         for (int r = q + 1; r < D; ++r) prod *= in[r];
       }
       pre *= in[q];
-      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, atanh_msg(prod, D - 1), total, lane);
+      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, atanh_msg(prod, D - 1), total, lane,
+                                 act, sk);
     }
   } else {
     T m1 = Num<T>::kBig, m2 = Num<T>::kBig, sgn = T(1);
@@ -196,7 +217,7 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
     for (int q = 0; q < D; ++q) {
       const T sign = ((negs >> q) & 1u) ? -sgn : sgn;
       const T out = D > 1 ? clampv(sign * (q == i1 ? m2 : m1)) : T(0);
-      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, out, total, lane);
+      strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, out, total, lane, act, sk);
     }
   }
 }
@@ -205,7 +226,7 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
 // reference's order (O(d^2) transcendental work; such checks are rare).
 template <typename T, int KERNEL, bool LAYERED>
 __device__ __noinline__ void strip_check_generic(const T* so, const T* st, const int* tv, int c, int k, int d,
-                                                 long long e0, int lane, T* c2v, T* total) {
+                                                 long long e0, int lane, T* c2v, T* total, bool act, SignSink& sk) {
   constexpr int F = kFixedFrames;
   for (int q = 0; q < d; ++q) {
     T out;
@@ -227,24 +248,27 @@ __device__ __noinline__ void strip_check_generic(const T* so, const T* st, const
       }
       out = d > 1 ? clampv(sign * mag) : T(0);
     }
-    strip_commit<T, LAYERED>(so, st, tv, q * k + c, e0, lane, out, c2v, total);
+    strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, (q * k + c) * F + lane, c2v + ((e0 + q * k + c) * F + lane), out,
+                               total, lane, act, sk);
   }
 }
 
 // The checks c = c0, c0 + step, ... of a staged strip (k checks, degree d).
 template <typename T, int KERNEL, bool LAYERED>
 __device__ __forceinline__ void strip_checks(const T* so, const T* st, const int* tv, int c0, int step, int k, int d,
-                                             long long e0, int lane, T* c2v, T* total) {
+                                             long long e0, int lane, T* c2v, T* total, bool act, SignSink& sk) {
   switch (d) {
-#define LDPC_SCK(D_)                                                                           \
-  case D_:                                                                                     \
-    for (int c = c0; c < k; c += step) strip_check_d<T, KERNEL, LAYERED, D_>(so, st, tv, c, k, e0, lane, c2v, total); \
+#define LDPC_SCK(D_)                                                                                     \
+  case D_:                                                                                               \
+    for (int c = c0; c < k; c += step)                                                                   \
+      strip_check_d<T, KERNEL, LAYERED, D_>(so, st, tv, c, k, e0, lane, c2v, total, act, sk);            \
     return;
     LDPC_SCK(1) LDPC_SCK(2) LDPC_SCK(3) LDPC_SCK(4) LDPC_SCK(5) LDPC_SCK(6) LDPC_SCK(7) LDPC_SCK(8)
     LDPC_SCK(9) LDPC_SCK(10) LDPC_SCK(11) LDPC_SCK(12) LDPC_SCK(13) LDPC_SCK(14) LDPC_SCK(15) LDPC_SCK(16)
 #undef LDPC_SCK
     default:
-      for (int c = c0; c < k; c += step) strip_check_generic<T, KERNEL, LAYERED>(so, st, tv, c, k, d, e0, lane, c2v, total);
+      for (int c = c0; c < k; c += step)
+        strip_check_generic<T, KERNEL, LAYERED>(so, st, tv, c, k, d, e0, lane, c2v, total, act, sk);
   }
 }
 
@@ -292,7 +316,7 @@ __device__ __forceinline__ int ld_acquire(const int* a) {
 // levels, with no grid-wide barrier or relaunch between levels.
 template <typename T, int KERNEL, bool LAYERED, int NC>
 __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::kMinBlocks)
-    phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int L0, int L1, int dep_base) {
+    phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int L0, int L1, int dep_base, int rev) {
   using L = TmaLayout<T, NC>;
   constexpr int F = kFixedFrames, S = kTmaStages, RPL = kTileEdges / 32;  // runs / rows per lane
   extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -317,7 +341,8 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x) {
         lm.seek(i);
-        if (p.amask[lm.group(i)]) break;
+        const int g = lm.group(i);
+        if (p.amask[rev ? p.groups - 1 - g : g]) break;
       }
       return i;
     };
@@ -328,8 +353,9 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     int vn[RPL];
     auto prefetch = [&](long long i) {
       if (i >= items) return;
-      grp = lm.group(i);
-      const int t = lm.strip(i, grp);
+      const int lg = lm.group(i);
+      const int t = lm.strip(i, lg);
+      grp = rev ? p.groups - 1 - lg : lg;
       need = dep_base + lm.P;
       rec = p.s_rec[t];
       nrun = p.s_rec[t + 1].w - rec.w;
@@ -409,20 +435,25 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
       lm.seek(it);
-      const int grp = lm.group(it);
+      const int lg = lm.group(it);
+      const int grp = rev ? p.groups - 1 - lg : lg;
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.s_rec[lm.strip(it, grp)];
+      const int4 rec = p.s_rec[lm.strip(it, lg)];
       GroupSlot<T> gs(p, grp);
       mbar_wait(&full[s], u & 1u);
-      if ((am >> lane) & 1u)
-        strip_checks<T, KERNEL, LAYERED>(so_of(s), st_of(s), tv_of(s), warp, NC, rec.y, rec.z, rec.x, lane, gs.c2v,
-                                         gs.total);
+      SignSink sk{gs.sign, p.k_info, LAYERED && p.layered_sign != 0, 0, 0};
+      strip_checks<T, KERNEL, LAYERED>(so_of(s), st_of(s), tv_of(s), warp, NC, rec.y, rec.z, rec.x, lane, gs.c2v,
+                                       gs.total, ((am >> lane) & 1u) != 0, sk);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (LAYERED) {
+        if (sk.errs) atomicAdd(&p.errs[grp * F + lane], sk.errs);
+        if (sk.ei) atomicAdd(&p.errs_info[grp * F + lane], sk.ei);
+      }
     }
   }
 }
@@ -454,7 +485,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x)
-        if (p.amask[(unsigned)i / (unsigned)nvs]) break;
+        if (p.amask[p.groups - 1 - (int)((unsigned)i / (unsigned)nvs)]) break;
       return i;
     };
     long long it = seek(blockIdx.x);
@@ -475,7 +506,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
-      GroupSlot<T> gs(p, (unsigned)it / (unsigned)nvs);
+      GroupSlot<T> gs(p, p.groups - 1 - (int)((unsigned)it / (unsigned)nvs));
       const int k = rec.y, erows = k * rec.z;
       T* sb = stage(s);
       if (lane == 0) {
@@ -496,13 +527,14 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
   } else {  // ---------------- consumers
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
-      const int grp = (int)((unsigned)it / (unsigned)nvs);
+      const int lgv = (int)((unsigned)it / (unsigned)nvs);
+      const int grp = p.groups - 1 - lgv;  // reverse group order: the check phase ends on the last groups
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.v_rec[(int)(it - (long long)grp * nvs)];
+      const int4 rec = p.v_rec[(int)(it - (long long)lgv * nvs)];
       GroupSlot<T> gs(p, grp);
       const bool act = (am >> lane) & 1u;
       const int k = rec.y, dv = rec.z;

@@ -46,6 +46,7 @@ struct ldpc_graph {
   DevGraph d;
   int* dev_block;  // one allocation for every device array
   int max_dv, max_dc, max_items;
+  int min_dv;  // 0 if some VN has no edge
   Tiling flood, layer;
   Strips sflood, slayer;
   int* strip_block;
@@ -82,8 +83,15 @@ struct HostStrips {
   std::vector<int> level_sptr, rec, runs, vn, vn_rows, v_rec, v_runs;
 };
 void build_strips(HostStrips& h, const std::vector<int>& lvl_ptr, const std::vector<int>& chk,
-                  const std::vector<int>& cn_ptr, const int* edge_vn, const std::vector<int>& vn_edges, int E) {
+                  const std::vector<int>& cn_ptr, const int* edge_vn, const std::vector<int>& vn_edges, int E,
+                  int N, bool mark_last) {
   std::vector<int> pos(E);
+  // mark_last: bit 31 of s_vn flags the row of each VN's last level (layered sign pass)
+  std::vector<int> last_level(N, -1);
+  if (mark_last)
+    for (size_t L = 0; L + 1 < lvl_ptr.size(); ++L)
+      for (int i = lvl_ptr[L]; i < lvl_ptr[L + 1]; ++i)
+        for (int e = cn_ptr[chk[i]]; e < cn_ptr[chk[i] + 1]; ++e) last_level[edge_vn[e]] = (int)L;
   h.level_sptr.push_back(0);
   int row = 0;
   for (size_t L = 0; L + 1 < lvl_ptr.size(); ++L) {
@@ -100,7 +108,7 @@ void build_strips(HostStrips& h, const std::vector<int>& lvl_ptr, const std::vec
         for (int c = 0; c < k; ++c) {
           const int e = cn_ptr[chk[i + c]] + q, r = q * k + c, v = edge_vn[e];
           pos[e] = row + r;
-          h.vn.push_back(v);
+          h.vn.push_back(mark_last && last_level[v] == (int)L ? (int)(0x80000000u | (unsigned)v) : v);
           if (open >= 0 && v == prev + 1 && (h.runs[open + 1] >> 8) < 255) {
             h.runs[open + 1] += 1 << 8;
           } else {
@@ -474,6 +482,12 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   // C2/C3 (the check kernel, not the relaunches, bounds the sweep), so off by default
   const char* fz = getenv("LDPC_LAYERED_FUSE");
   const bool fuse_levels = fz && !strcmp(fz, "1");
+  const char* ad = getenv("LDPC_ALT_DIR");  // alternate group order per level (default on)
+  const bool alt_dir = !(ad && !strcmp(ad, "0"));
+  // layered: sign words / error tallies from the check phase (every VN has an
+  // edge, so each VN's last-level commit sees its final total); LDPC_LAYERED_SIGN=0 off
+  const char* ls = getenv("LDPC_LAYERED_SIGN");
+  const bool layered_sign = layered && use_tma && G->min_dv > 0 && !(ls && !strcmp(ls, "0"));
   if (use_tma) {
     cudaFuncSetAttribute(K.check_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
     cudaFuncSetAttribute(K.vn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.vn_smem);
@@ -514,6 +528,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.iters = p.errs_info + pl.chunk * kFixedFrames;
     p.done = p.iters + pl.chunk * kFixedFrames;
     p.s_lvl = sp.lvl_sptr;
+    p.layered_sign = layered_sign ? 1 : 0;
     p.level_tptr = tl.level_tptr;
     p.tile_eptr = tl.tile_eptr;
     p.te_list = tl.te_list;
@@ -555,16 +570,18 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
       const int nlev = (int)lvl.size() - 1;
       if (use_tma && fuse_levels && nlev > 1) {
         // all levels in one launch; per-group dependency counters keep the order
-        int L0 = 0, L1 = nlev, dep = (it - 1) * lvl[nlev];
-        void* ac[] = {&p, &L0, &L1, &dep};
+        int L0 = 0, L1 = nlev, dep = (it - 1) * lvl[nlev], rev = 0;
+        void* ac[] = {&p, &L0, &L1, &dep, &rev};
         if (int rc = launch(K.check_tma, G_ * lvl[nlev], K.tma_smem, ac, K.tma_threads)) return rc;
       } else {
         for (int L = 0; L < nlev; ++L) {
           int t_lo = lvl[L], t_hi = lvl[L + 1];
           if (t_hi <= t_lo) continue;
           if (use_tma) {
-            int L0 = L, L1 = L + 1, dep = -1;
-            void* ac[] = {&p, &L0, &L1, &dep};
+            // alternate the group order level to level: a level starts on the
+            // groups the previous one ended with (their totals are L2-hot)
+            int L0 = L, L1 = L + 1, dep = -1, rev = (L & 1) && alt_dir ? 1 : 0;
+            void* ac[] = {&p, &L0, &L1, &dep, &rev};
             if (int rc = launch(K.check_tma, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
           } else {
             void* ac[] = {&p, &t_lo, &t_hi};
@@ -574,8 +591,8 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
       }
       if (use_tma && !layered) {
         if (int rc = launch(K.vn_tma, G_ * sp.n_vstrips, K.vn_smem, a1, K.vn_threads)) return rc;
-      } else if (int rc = launch(K.vn, G_ * vch, 0, a1)) {
-        return rc;
+      } else if (!layered_sign) {
+        if (int rc = launch(K.vn, G_ * vch, 0, a1)) return rc;
       }
       if (int rc = launch(K.syndrome, G_ * cch, 0, a1)) return rc;
       k = it;
@@ -1029,8 +1046,8 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     HostStrips hs[2];
     std::vector<int> all(M), one = {0, M}, ve(vn_edges, vn_edges + E), cp(cn_ptr, cn_ptr + M + 1);
     for (int m = 0; m < M; ++m) all[m] = m;
-    build_strips(hs[0], one, all, cp, edge_vn, ve, E);
-    build_strips(hs[1], level_ptr, level_checks, cp, edge_vn, ve, E);
+    build_strips(hs[0], one, all, cp, edge_vn, ve, E, N, false);
+    build_strips(hs[1], level_ptr, level_checks, cp, edge_vn, ve, E, N, true);
     build_vn_strips(hs[0], vn_ptr, N);
     std::vector<int> hb;
     size_t off[2][7];
@@ -1108,6 +1125,8 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
   }
   G->dev_block = d;
   G->max_dv = max_dv;
+  G->min_dv = N > 0 ? 1 << 30 : 0;
+  for (int n = 0; n < N; ++n) G->min_dv = std::min(G->min_dv, vn_ptr[n + 1] - vn_ptr[n]);
   G->max_dc = max_dc;
   G->max_items = (int)max_items;
   DevGraph& dg = G->d;

@@ -264,5 +264,7 @@ def test_layered_fused_levels_small_batches(count, precision):
     cfg = _cfg({"kind": "layered", "i_max": 4, "precision": precision})
     a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
     b = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
+    c = _with_env("LDPC_LAYERED_SIGN", "0", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
     for k in FIELDS:
         np.testing.assert_array_equal(a[k], b[k])
+        np.testing.assert_array_equal(a[k], c[k], err_msg=f"{k}: sign pass in the check phase vs separate VN pass")
