@@ -193,7 +193,9 @@ def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
             r = pyoracle.decode_batch(g, sample, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
                                       threads=cores)
             u = int(r["prop"].sum())
-            per[f"{kind}" + (f"/M{n_p}" if n_p > 1 else "")] = u / (time.perf_counter() - t1)
+            name = f"{kind}" + (f"/M{n_p}" if kind.startswith("me_") else "")
+            per[name] = {"updates_per_s": u / (time.perf_counter() - t1),
+                         "frame_errors": int((r["bit_errors_at"][:, -1] > 0).sum()), "frames": len(sample)}
             tot_u += u
         return tot_u, time.perf_counter() - t0, per
 
@@ -204,7 +206,17 @@ def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
         u, t, per = run(llr_host[:n].astype(np.float64))
     return {"value": u / t, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
             "sample": f"first {n} frames of the batch through every schedule ({t:.1f} s)",
-            "frames_per_s": n * len(scheds) / t, "per_schedule_updates_per_s": per}
+            "frames_per_s": n * len(scheds) / t,
+            "per_schedule_updates_per_s": {k: v["updates_per_s"] for k, v in per.items()},
+            "per_schedule_fer": {k: (v["frame_errors"], v["frames"]) for k, v in per.items()}}
+
+
+def clopper_pearson(k, n, alpha=0.05):
+    """Exact two-sided binomial confidence interval (FER CI, north star)."""
+    from scipy.stats import beta
+    lo = 0.0 if k == 0 else float(beta.ppf(alpha / 2, k, n - k + 1))
+    hi = 1.0 if k == n else float(beta.ppf(1 - alpha / 2, k + 1, n - k))
+    return lo, hi
 
 
 def run_ours(args, wl):
@@ -347,7 +359,16 @@ def run_ours(args, wl):
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(wl, spec, g, llr_host, budget_s=args.cpu_budget)
+        cb = cpu_baseline(wl, spec, g, llr_host, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cb
+        # FER vs oracle: the GPU's FER over the whole batch must lie inside the
+        # oracle sample's 95 % Clopper-Pearson interval (north star)
+        for nm, (k, n) in cb["per_schedule_fer"].items():
+            if nm in per:
+                lo, hi = clopper_pearson(k, n)
+                per[nm]["oracle_fer_sample"] = k / n
+                per[nm]["oracle_fer_ci95"] = [lo, hi]
+                per[nm]["fer_inside_oracle_ci95"] = bool(lo <= per[nm]["fer"] <= hi)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

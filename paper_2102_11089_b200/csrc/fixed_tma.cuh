@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
         if (q == s) pub[q] = grp;
       it = seek(it + gridDim.x);
       prefetch(it);
+      if (dep_base >= 0) publish_upto(kk, false);  // eagerly
     }
     if (dep_base >= 0) publish_upto(kk, true);  // drain: the items still in flight
   } else {  // ---------------- consumers
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
     }
   }
 }
+
 
 #endif  // LDPC_PHASE_DECL_ONLY
 

@@ -478,8 +478,11 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   // check phase: the TMA-fed warp-specialised kernel unless LDPC_PHASE_CHECK=legacy
   const bool use_tma = phase_use_tma(s);
   // layered: LDPC_LAYERED_FUSE=1 runs all levels in one check launch ordered by
-  // per-group dependency counters; measured equal to one launch per level on
-  // C2/C3 (the check kernel, not the relaunches, bounds the sweep), so off by default
+  // per-group dependency counters; measured within 3 % of one launch per level on
+  // C2/C3 (the check kernel's DRAM traffic, not the relaunches, bounds the sweep),
+  // and it relies on every CTA of the grid being co-resident, so off by default.
+  // (Fusing the flooding check and VN phases the same way, for L2 reuse of the
+  // fresh c2v rows, measured 1.5x slower: VN items stall on the slowest CTA.)
   const char* fz = getenv("LDPC_LAYERED_FUSE");
   const bool fuse_levels = fz && !strcmp(fz, "1");
   const char* ad = getenv("LDPC_ALT_DIR");  // alternate group order per level (default on)
