@@ -483,10 +483,12 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
   __syncthreads();
   const int nvs = p.n_vstrips;
   const long long items = (long long)p.groups * nvs;
+  // optional reverse group order (the check phase ends on the last groups)
+  auto vgrp = [&](int g) { return p.vn_reverse ? p.groups - 1 - g : g; };
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x)
-        if (p.amask[p.groups - 1 - (int)((unsigned)i / (unsigned)nvs)]) break;
+        if (p.amask[vgrp((int)((unsigned)i / (unsigned)nvs))]) break;
       return i;
     };
     long long it = seek(blockIdx.x);
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       if (kk >= S) mbar_wait(&empty[s], (u - 1) & 1u);
-      GroupSlot<T> gs(p, p.groups - 1 - (int)((unsigned)it / (unsigned)nvs));
+      GroupSlot<T> gs(p, vgrp((int)((unsigned)it / (unsigned)nvs)));
       const int k = rec.y, erows = k * rec.z;
       T* sb = stage(s);
       if (lane == 0) {
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(VnLayout<T, NC>::kThreads, sizeof(T) == 4 ? 2 
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
       const int lgv = (int)((unsigned)it / (unsigned)nvs);
-      const int grp = p.groups - 1 - lgv;  // reverse group order: the check phase ends on the last groups
+      const int grp = vgrp(lgv);
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;

@@ -489,6 +489,8 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   const bool alt_dir = !(ad && !strcmp(ad, "0"));
   // layered: sign words / error tallies from the check phase (every VN has an
   // edge, so each VN's last-level commit sees its final total); LDPC_LAYERED_SIGN=0 off
+  const char* vr = getenv("LDPC_VN_REVERSE");  // flooding VN phase in reverse group order (opt-in)
+  const bool vn_rev = vr && !strcmp(vr, "1");
   const char* ls = getenv("LDPC_LAYERED_SIGN");
   const bool layered_sign = layered && use_tma && G->min_dv > 0 && !(ls && !strcmp(ls, "0"));
   if (use_tma) {
@@ -532,6 +534,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.done = p.iters + pl.chunk * kFixedFrames;
     p.s_lvl = sp.lvl_sptr;
     p.layered_sign = layered_sign ? 1 : 0;
+    p.vn_reverse = vn_rev ? 1 : 0;
     p.level_tptr = tl.level_tptr;
     p.tile_eptr = tl.tile_eptr;
     p.te_list = tl.te_list;
