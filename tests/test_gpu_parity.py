@@ -268,3 +268,35 @@ def test_layered_fused_levels_small_batches(count, precision):
     for k in FIELDS:
         np.testing.assert_array_equal(a[k], b[k])
         np.testing.assert_array_equal(a[k], c[k], err_msg=f"{k}: sign pass in the check phase vs separate VN pass")
+
+
+@pytest.mark.parametrize("kind", ["rbp", "cirbp", "lmdrbp", "me_cirbp"])
+def test_fp32_messages_within_1e4_first_1000_updates(kind):
+    """North-star fp32 bar: over the first 1000 updates, the fp32 decoder's
+    committed C2V values agree with the float64 reference arithmetic within
+    1e-4 relative (absolute 1e-4 for |c2v| < 1).  Compared update by update
+    while both runs propagate the same edge; a run may leave the common path
+    only at a float64 near-tie (fp32 rounding flips the argmax), after which
+    the states legitimately differ."""
+    from paper_2102_11089_b200.schedules import decode_batch_logged
+    spec, g = load_code("C0")
+    llrs = llr_batch(spec, 2.0, seed=21, start=0, count=64)
+    cfg64 = _cfg({"kind": kind, "i_max": 5, "n_p": 4})
+    cfg32 = _cfg({"kind": kind, "i_max": 5, "n_p": 4, "precision": "f32"})
+    t = torch.from_numpy(llrs).cuda()
+    a = decode_batch_logged(spec, t, cfg64, log_cap=1000)
+    b = decode_batch_logged(spec, t, cfg32, log_cap=1000)
+    torch.cuda.synchronize()
+    ea, eb = a["step_log"].cpu().numpy(), b["step_log"].cpu().numpy()
+    va, vb = a["step_c2v"].cpu().numpy(), b["step_c2v"].cpu().numpy()
+    compared, diverged = 0, 0
+    for f in range(len(llrs)):
+        same = (ea[f] == eb[f]) & (ea[f] >= 0)
+        n = len(same) if same.all() else int(np.argmin(same))  # common prefix
+        if n < len(same) and ea[f][n] >= 0:
+            diverged += 1
+        x, y = va[f][:n], vb[f][:n]
+        np.testing.assert_array_less(np.abs(x - y), 1e-4 * np.maximum(np.abs(x), 1.0) + 1e-12,
+                                     err_msg=f"{kind} frame {f}")
+        compared += n
+    assert compared >= 0.8 * 64 * 1000, (compared, diverged)
