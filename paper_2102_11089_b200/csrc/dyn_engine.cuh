@@ -1134,6 +1134,65 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
   c.w.sync();
 }
 
+// ME-RBP round selection on a single-level residual tree: the top-m leaves by
+// (key desc, index asc) -- the set m repeated argmax-and-exclude passes pick
+// (oracle decode_me_rbp).  Any leaf of that set lies in one of the top-m
+// level-1 groups ordered by (group max, group index): otherwise m groups rank
+// above its own group, and their maxima are m leaves ranking above it.
+template <typename T, int G, typename LeafFn>
+__device__ void me_topm_registers(const DynParams& p, Ctx<T, G>& c, int m, LeafFn leaf) {
+  using Key = typename Num<T>::Key;
+  constexpr int kBad = 0x7fffffff;
+  const int lane = c.lane, s = p.rgeo.size[1], E = p.g.E;
+  const Key* L1 = c.rtree + p.rgeo.off[1];
+  Key k0 = lane < s ? L1[lane] : Key(0), k1 = lane + 32 < s ? L1[lane + 32] : Key(0);
+  bool v0 = lane < s, v1 = lane + 32 < s;
+  int gq[4] = {kBad, kBad, kBad, kBad};
+  int ng = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (t >= m) break;
+    Key bk = 0;
+    int bi = kBad;
+    if (v0) { bk = k0; bi = lane; }
+    if (v1 && (bi == kBad || k1 > bk)) { bk = k1; bi = lane + 32; }
+    int q;
+    c.w.max_key_minidx(bk, bi, &q);
+    if (q == kBad) break;
+    gq[t] = q;
+    ++ng;
+    if (q == lane) v0 = false;
+    if (q == lane + 32) v1 = false;
+  }
+  Key ck[4];
+  int ce[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int e = j < ng ? gq[j] * 32 + lane : E;
+    ce[j] = e < E ? e : kBad;
+    ck[j] = e < E ? leaf(e) : Key(0);
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (t >= m) break;
+    Key bk = 0;
+    int bi = kBad;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ce[j] != kBad && (bi == kBad || ck[j] > bk || (ck[j] == bk && ce[j] < bi))) {
+        bk = ck[j];
+        bi = ce[j];
+      }
+    int e;
+    c.w.max_key_minidx(bk, bi, &e);
+    if (lane == 0) c.sel[t] = e;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ce[j] == e) ce[j] = kBad;
+  }
+  c.w.sync();
+}
+
 template <typename T, int KERNEL, int KF, int G, bool TR>
 __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
@@ -1311,6 +1370,21 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       tree_build(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
       int boundary = 1;
       const int np_ = p.n_p < g.E ? p.n_p : g.E;
+      // single-level residual tree (<= 64 groups of 32 leaves) and M <= 4: the
+      // round's top-M set in registers -- top-M groups by (max key, index),
+      // which must contain the top-M leaves, then top-M among their leaves --
+      // instead of M argmax / exclude / recompute passes over the tree
+      const bool reg_topm = G == 32 && p.rgeo.levels == 1 && np_ <= 4;
+      while (boundary <= I && !conv && reg_topm) {
+        me_topm_registers<T, G>(p, c, np_, sleaf);
+        c.cnt[C_CMP] += E - 1;
+        sort_small<T, G>(c, c.sel, np_);
+        for (int idx = 0; idx < np_; ++idx) {
+          propagate<T, KERNEL, false, true, false, true, G, false, TR>(p, c, c.sel[idx]);
+          ++c.prop;
+        }
+        me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
+      }
       while (boundary <= I && !conv) {
         for (int t = 0; t < np_; ++t) {
           int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
