@@ -67,6 +67,7 @@ struct PhaseParams {
   const int* s_lvl;  // [levels + 1] first strip of each level (check strips)
   int layered_sign;  // layered: sign words / error tallies from the check phase (no VN pass)
   int vn_reverse;    // flooding VN phase in reverse group order
+  int lwin;          // layered, levels fused: groups per window (0 = all groups)
   int* done;         // [groups] committed check strips per group (layered, levels fused in one launch)
 };
 

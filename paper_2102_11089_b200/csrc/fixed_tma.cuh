@@ -279,25 +279,49 @@ __device__ __forceinline__ void strip_checks(const T* so, const T* st, const int
 // dependencies (the group's earlier levels) come earlier in the order.
 struct LevelMap {
   const int* lp;  // strip prefix per level (lp[L] = first strip of level L)
-  int L, L1, G, P, nL;
-  long long lo, hi;  // item range of level L
-  __device__ LevelMap(const int* lp_, int L0, int L1_, int G_) : lp(lp_), L(L0), L1(L1_), G(G_) {
-    lo = 0;
+  int L0, L1, G, W, Ptot;
+  long long wlo, whi;  // item range of the current window of groups [gb, gb + Gw)
+  int gb, Gw;
+  int L, P, nL;
+  long long lo, hi;  // item range of level L within the window
+  // Items: windows of W consecutive groups; inside a window level-major, then
+  // group, then strip (W = G: the plain level-major order).
+  __device__ LevelMap(const int* lp_, int L0_, int L1_, int G_, int W_) : lp(lp_), L0(L0_), L1(L1_), G(G_) {
+    W = (W_ <= 0 || W_ > G) ? G : W_;
+    Ptot = lp[L1] - lp[L0];
+    gb = 0;
+    Gw = W < G ? W : G;
+    wlo = 0;
+    whi = (long long)Gw * Ptot;
+    start_level();
+  }
+  __device__ __forceinline__ void start_level() {
+    L = L0;
+    lo = wlo;
     P = lp[L];
     nL = lp[L + 1] - P;
-    hi = (long long)G * nL;
+    hi = lo + (long long)Gw * nL;
   }
   __device__ __forceinline__ void seek(long long i) {
+    while (i >= whi && gb + Gw < G) {
+      gb += Gw;
+      Gw = G - gb < W ? G - gb : W;
+      wlo = whi;
+      whi = wlo + (long long)Gw * Ptot;
+      start_level();
+    }
     while (i >= hi && L + 1 < L1) {
       ++L;
       lo = hi;
       P = lp[L];
       nL = lp[L + 1] - P;
-      hi = lo + (long long)G * nL;
+      hi = lo + (long long)Gw * nL;
     }
   }
-  __device__ __forceinline__ int group(long long i) const { return (int)((unsigned)(i - lo) / (unsigned)nL); }
-  __device__ __forceinline__ int strip(long long i, int g) const { return P + (int)(i - lo - (long long)g * nL); }
+  __device__ __forceinline__ int group(long long i) const { return gb + (int)((unsigned)(i - lo) / (unsigned)nL); }
+  __device__ __forceinline__ int strip(long long i, int g) const {
+    return P + (int)(i - lo - (long long)(g - gb) * nL);
+  }
 };
 
 __device__ __forceinline__ int ld_acquire(const int* a) {
@@ -335,7 +359,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
   }
   __syncthreads();
   const long long items = (long long)p.groups * (p.s_lvl[L1] - p.s_lvl[L0]);  // < 2^31
-  LevelMap lm(p.s_lvl, L0, L1, p.groups);
+  LevelMap lm(p.s_lvl, L0, L1, p.groups, dep_base >= 0 ? p.lwin : 0);
 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {

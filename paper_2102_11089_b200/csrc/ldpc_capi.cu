@@ -485,6 +485,8 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   // fresh c2v rows, measured 1.5x slower: VN items stall on the slowest CTA.)
   const char* fz = getenv("LDPC_LAYERED_FUSE");
   const bool fuse_levels = fz && !strcmp(fz, "1");
+  const char* lw = getenv("LDPC_LAYERED_WINDOW");  // fused levels: groups per window (L2 reuse of totals)
+  const int lwin = lw ? atoi(lw) : 0;
   const char* ad = getenv("LDPC_ALT_DIR");  // alternate group order per level (default on)
   const bool alt_dir = !(ad && !strcmp(ad, "0"));
   // layered: sign words / error tallies from the check phase (every VN has an
@@ -535,6 +537,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.s_lvl = sp.lvl_sptr;
     p.layered_sign = layered_sign ? 1 : 0;
     p.vn_reverse = vn_rev ? 1 : 0;
+    p.lwin = lwin;
     p.level_tptr = tl.level_tptr;
     p.tile_eptr = tl.tile_eptr;
     p.te_list = tl.te_list;

@@ -300,3 +300,18 @@ def test_fp32_messages_within_1e4_first_1000_updates(kind):
                                      err_msg=f"{kind} frame {f}")
         compared += n
     assert compared >= 0.8 * 64 * 1000, (compared, diverged)
+
+
+@pytest.mark.parametrize("window", [1, 2, 3])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_layered_fused_levels_group_windows(window, precision):
+    """Levels fused, items ordered in windows of `window` groups (level-major
+    inside a window): same answers as one launch per level."""
+    spec, g = load_code("C2")
+    llrs = llr_batch(spec, 1.0, seed=4, start=0, count=200)
+    cfg = _cfg({"kind": "layered", "i_max": 3, "precision": precision})
+    a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
+    b = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env(
+        "LDPC_LAYERED_WINDOW", str(window), lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))))
+    for k in FIELDS:
+        np.testing.assert_array_equal(a[k], b[k])
