@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
       mbar_wait(&full[s], u & 1u);
       SignSink sk{gs.sign, p.k_info, LAYERED && p.layered_sign != 0, 0, 0};
       const bool act = ((am >> lane) & 1u) != 0;
-      if (LAYERED && sk.on) {  // every lane takes part (sign ballots)
+      if (LAYERED) {  // every lane takes part (the sign ballots need the whole warp)
         strip_checks<T, KERNEL, LAYERED>(so_of(s), st_of(s), tv_of(s), warp, NC, rec.y, rec.z, rec.x, lane, gs.c2v,
                                          gs.total, act, sk);
       } else if (act) {
