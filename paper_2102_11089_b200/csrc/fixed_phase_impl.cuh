@@ -9,7 +9,8 @@
 template <typename T, int KERNEL, int NC>
 static void* tma_check_of(int layered) {
   using namespace ldpc;
-  return layered ? (void*)phase_check_tma_kernel<T, KERNEL, true, NC> : (void*)phase_check_tma_kernel<T, KERNEL, false, NC>;
+  return layered ? (void*)phase_check_tma_kernel<T, KERNEL, true, NC, false>
+                 : (void*)phase_check_tma_kernel<T, KERNEL, false, NC, false>;
 }
 
 // NC0 / NC1: consumer-warp counts built for this type (LDPC_TMA_CONSUMERS picks NC1)
@@ -33,6 +34,9 @@ static void ldpc_phase_fill(PhaseKernels& k, int kernel, int layered) {
   k.tma_threads = alt ? TmaLayout<T, NC1>::kThreads : TmaLayout<T, NC0>::kThreads;
   k.tma_smem = TmaLayout<T, NC0>::kBytes;
   k.vn_tma = (void*)phase_vn_tma_kernel<T, 8>;
+  // layered with all levels in one launch (LDPC_LAYERED_FUSE=1)
+  k.check_tma_fused = kernel == KERNEL_EXACT ? (void*)phase_check_tma_kernel<T, KERNEL_EXACT, true, NC0, true>
+                                             : (void*)phase_check_tma_kernel<T, KERNEL_MINSUM, true, NC0, true>;
   k.vn_threads = VnLayout<T, 8>::kThreads;
   k.vn_smem = VnLayout<T, 8>::kBytes;
 }

@@ -338,7 +338,12 @@ __device__ __forceinline__ int ld_acquire(const int* a) {
 // committed (one release-increment per finished item) -- the level order of
 // the reference sweep is kept per group while different groups run different
 // levels, with no grid-wide barrier or relaunch between levels.
-template <typename T, int KERNEL, bool LAYERED, int NC>
+// FUSED: the build with the level map, dependency waits and item publication
+// (all layered levels in one launch when dep_base >= 0; with dep_base < 0 it
+// runs one level like the plain build -- the layered per-level launches use
+// it because ptxas allocates it without spills); the plain build (flooding)
+// maps the items of one level range directly.
+template <typename T, int KERNEL, bool LAYERED, int NC, bool FUSED>
 __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::kMinBlocks)
     phase_check_tma_kernel(const __grid_constant__ PhaseParams p, int L0, int L1, int dep_base, int rev) {
   using L = TmaLayout<T, NC>;
@@ -358,14 +363,25 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     mbar_fence_init();
   }
   __syncthreads();
-  const long long items = (long long)p.groups * (p.s_lvl[L1] - p.s_lvl[L0]);  // < 2^31
-  LevelMap lm(p.s_lvl, L0, L1, p.groups, dep_base >= 0 ? p.lwin : 0);
+  const int t0 = p.s_lvl[L0], nti = p.s_lvl[L1] - t0;
+  const long long items = (long long)p.groups * nti;  // < 2^31
+  LevelMap lm(p.s_lvl, L0, FUSED ? L1 : L0 + 1, p.groups, FUSED && dep_base >= 0 ? p.lwin : 0);
+  // item -> (logical group, strip)
+  auto item_group = [&](long long i) -> int {
+    if (FUSED) {
+      lm.seek(i);
+      return lm.group(i);
+    }
+    return (int)((unsigned)i / (unsigned)nti);
+  };
+  auto item_strip = [&](long long i, int lg) -> int {
+    return FUSED ? lm.strip(i, lg) : t0 + (int)(i - (long long)lg * nti);
+  };
 
   if (warp == NC) {  // ---------------- producer
     auto seek = [&](long long i) {
       for (; i < items; i += gridDim.x) {
-        lm.seek(i);
-        const int g = lm.group(i);
+        const int g = item_group(i);
         if (p.amask[rev ? p.groups - 1 - g : g]) break;
       }
       return i;
@@ -377,10 +393,10 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     int vn[RPL];
     auto prefetch = [&](long long i) {
       if (i >= items) return;
-      const int lg = lm.group(i);
-      const int t = lm.strip(i, lg);
+      const int lg = item_group(i);
+      const int t = item_strip(i, lg);
       grp = rev ? p.groups - 1 - lg : lg;
-      need = dep_base + lm.P;
+      if (FUSED) need = dep_base + lm.P;
       rec = p.s_rec[t];
       nrun = p.s_rec[t + 1].w - rec.w;
 #pragma unroll
@@ -405,7 +421,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
         const unsigned par = (unsigned)(pub_k / S) & 1u;
         if (block) mbar_wait(&empty[s], par);
         else if (!mbar_test(&empty[s], par)) return;
-        if (dep_base >= 0 && lane == 0) {
+        if (FUSED && dep_base >= 0 && lane == 0) {
           int g = 0;
 #pragma unroll
           for (int q = 0; q < S; ++q)
@@ -418,7 +434,10 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
     };
     for (; it < items; ++kk) {
       const int s = kk % S;
-      if (kk >= S) publish_upto(kk - S + 1, true);  // stage s is free (and its item published)
+      if (kk >= S) {  // stage s must be free (fused: and its item published)
+        if (FUSED) publish_upto(kk - S + 1, true);
+        else mbar_wait(&empty[s], (unsigned)(kk / S - 1) & 1u);
+      }
       GroupSlot<T> gs(p, grp);
       const int rows = rec.y * rec.z;
       if (LAYERED) {
@@ -427,7 +446,7 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
         for (int j = 0; j < RPL; ++j)
           if (lane + 32 * j < rows) tv[lane + 32 * j] = vn[j];
       }
-      if (dep_base >= 0) {  // the group's earlier levels must be committed
+      if (FUSED && dep_base >= 0) {  // the group's earlier levels must be committed
         while (ld_acquire(p.done + grp) < need) {
           publish_upto(kk, false);
           __nanosleep(32);
@@ -448,26 +467,27 @@ __global__ void __launch_bounds__(TmaLayout<T, NC>::kThreads, TmaLayout<T, NC>::
           bulk_g2s(st + row * F, gs.total + (long long)run[j].x * F, len * L::kRowBytes, &full[s]);
         }
       }
+      if (FUSED) {
 #pragma unroll
-      for (int q = 0; q < S; ++q)
-        if (q == s) pub[q] = grp;
+        for (int q = 0; q < S; ++q)
+          if (q == s) pub[q] = grp;
+      }
       it = seek(it + gridDim.x);
       prefetch(it);
-      if (dep_base >= 0) publish_upto(kk, false);  // eagerly
+      if (FUSED) publish_upto(kk, false);  // eagerly
     }
-    if (dep_base >= 0) publish_upto(kk, true);  // drain: the items still in flight
+    if (FUSED) publish_upto(kk, true);  // drain: the items still in flight
   } else {  // ---------------- consumers
     long long it = blockIdx.x;
     for (int kk = 0; it < items; it += gridDim.x) {
-      lm.seek(it);
-      const int lg = lm.group(it);
+      const int lg = item_group(it);
       const int grp = rev ? p.groups - 1 - lg : lg;
       const unsigned am = p.amask[grp];
       if (!am) continue;
       const int s = kk % S;
       const unsigned u = (unsigned)(kk / S);
       ++kk;
-      const int4 rec = p.s_rec[lm.strip(it, lg)];
+      const int4 rec = p.s_rec[item_strip(it, lg)];
       GroupSlot<T> gs(p, grp);
       mbar_wait(&full[s], u & 1u);
       SignSink sk{gs.sign, p.k_info, LAYERED && p.layered_sign != 0, 0, 0};

@@ -66,6 +66,7 @@ void* ldpc_fixed_trace_kernel(int f64, int kernel, int layered);
 struct PhaseKernels {
   void *init, *check, *vn, *syndrome, *finalize, *output;
   void* check_tma;           // warp-specialised TMA-fed check phase (fixed_tma.cuh)
+  void* check_tma_fused;     // same, layered levels in one launch (dependency counters)
   int tma_threads, tma_smem;
   void* vn_tma;              // TMA-fed VN phase over VN strips (flooding)
   int vn_threads, vn_smem;

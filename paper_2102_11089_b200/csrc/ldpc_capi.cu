@@ -498,6 +498,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   if (use_tma) {
     cudaFuncSetAttribute(K.check_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
     cudaFuncSetAttribute(K.vn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.vn_smem);
+    cudaFuncSetAttribute(K.check_tma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
   }
   auto grid_of = [&](void* fn, int smem, long long items, int threads = kPhaseThreads) {
     int occ = 0;
@@ -581,7 +582,7 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
         // all levels in one launch; per-group dependency counters keep the order
         int L0 = 0, L1 = nlev, dep = (it - 1) * lvl[nlev], rev = 0;
         void* ac[] = {&p, &L0, &L1, &dep, &rev};
-        if (int rc = launch(K.check_tma, G_ * lvl[nlev], K.tma_smem, ac, K.tma_threads)) return rc;
+        if (int rc = launch(K.check_tma_fused, G_ * lvl[nlev], K.tma_smem, ac, K.tma_threads)) return rc;
       } else {
         for (int L = 0; L < nlev; ++L) {
           int t_lo = lvl[L], t_hi = lvl[L + 1];
@@ -591,7 +592,9 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
             // groups the previous one ended with (their totals are L2-hot)
             int L0 = L, L1 = L + 1, dep = -1, rev = (L & 1) && alt_dir ? 1 : 0;
             void* ac[] = {&p, &L0, &L1, &dep, &rev};
-            if (int rc = launch(K.check_tma, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
+            // layered: the FUSED build (spill-free allocation), one level per launch
+            void* fn = layered && !getenv("LDPC_TMA_CONSUMERS") ? K.check_tma_fused : K.check_tma;
+            if (int rc = launch(fn, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
           } else {
             void* ac[] = {&p, &t_lo, &t_hi};
             if (int rc = launch(K.check, G_ * (t_hi - t_lo), pl.smem_check, ac)) return rc;
