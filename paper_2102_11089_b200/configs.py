@@ -79,14 +79,41 @@ def bg2_shaped_base_graph(seed=2, rows=42, cols=52, z=52, n_sys=10, p_core=0.7,
     return _to_bg(g, z)
 
 
+def _encodable_core_block(g, rng, n_sys, z):
+    """4x4 double-diagonal core in the NR form: first core column of weight 3
+    (rows 0,1,3) with shifts (a, b, a), staircase columns with identity
+    circulants.  Summing the four core rows cancels the staircase and the two
+    equal circulants of the first column, leaving P^b: the core block is
+    invertible, so the core parity is a function of the systematic bits."""
+    c = n_sys
+    a, b = (int(x) for x in rng.integers(z, size=2))
+    g[0, c], g[1, c], g[3, c] = a, b, a
+    for k, (r0, r1) in enumerate(((0, 1), (1, 2), (2, 3)), start=1):
+        g[r0, c + k] = 0
+        g[r1, c + k] = 0
+
+
 def bg1_shaped_base_graph(seed=3, rows=46, cols=68, z=384, n_sys=22, sys_weight_mean=8.5,
-                          target_nnz=316, ext_max=9):
+                          target_nnz=316, ext_max=9, core_hits=(3, 4), heavy_punct=True):
     """C3: 46x68, Z=384.  22 systematic columns with seeded weights averaging
     8.5, 4x4 double-diagonal core, 42 weight-1 extension parity columns,
-    extension rows with 3-10 nonzeros, about 316 base nonzeros in total."""
+    extension rows with 3-10 nonzeros, about 316 base nonzeros in total.
+
+    As in NR BG1, the four core rows are dense in the systematic columns: every
+    systematic column has 3 or 4 (seeded) of its entries in core rows 0-3 and
+    the rest in extension rows.  A systematic column without core-row entries
+    would be a low-weight codeword by itself (the bit plus the weight-1
+    extension parity bits of its rows); the round-1 generator, which only
+    weighted core rows 4x in a random draw, left columns 6 and 17 so, giving
+    weight-5/6 codewords and an FER of 1.0 (Weak 1).  Also as in
+    NR BG1, the two punctured columns (0 and 1) take the two largest of the
+    seeded weights (punctured VNs of low degree stall decoding).  Shifts of
+    systematic and extension entries stay uniform in [0, Z).  Oracle check
+    (layered, 128-256 seeded frames): 3.0 dB / i_max 30 converges to the
+    all-zero word on every frame; 1.0 dB / i_max 10 FER 0.91; 1.5 dB FER 0."""
     rng = np.random.default_rng(seed)
     g = _grid(rows, cols)
-    _core_block(g, rng, n_sys, z)
+    _encodable_core_block(g, rng, n_sys, z)
     for r in range(4, rows):
         g[r, n_sys + 4 + (r - 4)] = rng.integers(z)
     # systematic column weights: seeded, clipped to [3, 16], total = round(mean * n_sys)
@@ -98,20 +125,26 @@ def bg1_shaped_base_graph(seed=3, rows=46, cols=68, z=384, n_sys=22, sys_weight_
             w[j] += 1
         elif w.sum() > total_w and w[j] > 3:
             w[j] -= 1
+    if heavy_punct:
+        # the two punctured columns carry the two largest weights (NR BG1 form)
+        top = np.argsort(-w, kind="stable")[:2]
+        rest = [j for j in range(n_sys) if j not in set(top.tolist())]
+        w = np.concatenate([w[top], w[rest]])
     ext_rows = np.arange(4, rows)
 
     def ext_load(r):
         return int((g[r, :n_sys + 4] >= 0).sum())
 
-    # core rows are dense in systematic columns (4x the weight of an extension row)
-    p = np.ones(rows)
-    p[:4] = 4.0
+    # core rows: 3-4 seeded entries per systematic column; extension rows: the rest
     for j in range(n_sys):
-        ok = np.array([(r < 4) or ext_load(r) < ext_max for r in range(rows)], dtype=float)
-        q = p * ok
-        sel = rng.choice(rows, size=int(w[j]), replace=False, p=q / q.sum())
-        for r in sel:
+        n_core = int(min(w[j], rng.integers(core_hits[0], core_hits[1] + 1)))
+        for r in rng.choice(4, size=n_core, replace=False):
             g[r, j] = rng.integers(z)
+        n_ext = int(w[j]) - n_core
+        ok = np.array([ext_load(r) < ext_max for r in ext_rows], dtype=float)
+        if n_ext:
+            for r in rng.choice(ext_rows, size=n_ext, replace=False, p=ok / ok.sum()):
+                g[r, j] = rng.integers(z)
     # top up the extension rows with core-column entries until ~target_nnz
     # (rows with the fewest non-identity entries first; at least 2 per row)
     while int((g >= 0).sum()) < target_nnz or min(ext_load(r) for r in ext_rows) < 2:

@@ -110,8 +110,11 @@ def plan():
     cases.append(("c1", "C1", 2.0, 24, True, [dict(kind=k, i_max=3, n_p=4) for k in ref8]))
     c2 = [dict(kind=k, i_max=3, n_p=4) for k in ref8] + [dict(kind="me_cirbp", i_max=3, n_p=16)]
     cases.append(("c2", "C2", 1.0, 6, True, c2))
-    c3 = [dict(kind=k, i_max=2, n_p=64) for k in ("flooding", "rbp", "cirbp", "lmd_cirbp", "me_cirbp")]
-    cases.append(("c3", "C3", 1.0, 2, False, c3))
+    # C3 at BASELINE configs[3]'s own budget (i_max 10) and both of its SNRs
+    c3 = [dict(kind=k, i_max=10, n_p=64) for k in ("flooding", "rbp", "cirbp", "me_cirbp")]
+    c3 += [dict(kind="lmd_cirbp", i_max=2), dict(kind="rbp", i_max=2, kernel="minsum")]
+    cases.append(("c3", "C3", 1.0, 16, False, c3))
+    cases.append(("c3b", "C3", 0.5, 16, False, c3[:4]))
     return cases
 
 
@@ -202,8 +205,11 @@ def main():
     mine = configs.make_c0_code()
     assert ref_c0.h.entries == mine.h.entries, "C0 constructor drifted from the reference"
     rng = np.random.default_rng(2102_11089)
+    only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     with ProcessPoolExecutor(max_workers=os.cpu_count()) as pool:
         for fname, key, ebn0, nfr, ties, scheds in plan():
+            if only and fname not in only:
+                continue
             spec = {"C0": configs.make_c0_code, "C1": configs.make_c1_code,
                     "C2": configs.make_c2_code, "C3": configs.make_c3_code}[key]()
             llrs = llr_batch(spec, ebn0, seed=0, start=0, count=nfr, dtype=np.float32)
@@ -226,6 +232,8 @@ def main():
             np.savez_compressed(OUT / f"{fname}.npz", **payload)
             print(f"{fname}: {len(scheds)} schedules x {len(llrs)} frames  ({time.time() - t0:.0f}s)",
                   flush=True)
+    if only:
+        return
     # KATs (SPEC.md examples, evaluated by the reference)
     from ldpc_ids import kernels as rk, schedules as rs, _engine as re_
     kat = {}

@@ -25,7 +25,7 @@ def trace(spec, g, llrs, cfg, frames, placement="auto", tol=NEAR_TIE):
     frames = list(frames)
     if not frames:
         return []
-    cap = int(min(cfg.i_max * g.n_edges + max(cfg.n_p, 1), 60_000))
+    cap = int(min(cfg.i_max * g.n_edges + max(cfg.n_p, 1), 2_000_000))
     sub = np.ascontiguousarray(llrs[frames])
     out = decode_batch_logged(spec, torch.from_numpy(sub).cuda(), cfg, log_cap=cap, placement=placement)
     torch.cuda.synchronize()

@@ -6,6 +6,7 @@ tests/golden/*.npz (tests/golden/make_golden.py).
 """
 
 import ast
+import os
 
 import numpy as np
 import pytest
@@ -24,10 +25,16 @@ def test_oracle_matches_reference_golden(fname, code_key, si, sched):
     cfg = dict(kind="flooding", gamma=0.1, n_p=1, n_g=16, i_max=3, kernel="exact",
                selection_seed=0)
     cfg.update(sched)
+    # BG1 cases at i_max 10 cost seconds per frame on the CPU: the oracle is
+    # pinned on the first 8 of their 16 frames here (the GPU tests compare the
+    # CUDA decoder with all 16 reference frames directly)
+    nf = 8 if code_key == "C3" and cfg["i_max"] > 2 else len(llrs)
+    llrs = llrs[:nf]
     out = pyoracle.decode_batch(g, llrs, cfg["kind"], cfg["kernel"], cfg["i_max"], spec.k_info,
                                 cfg["gamma"], cfg["n_p"], cfg["n_g"], cfg["selection_seed"],
-                                threads=4)
+                                threads=os.cpu_count())
     t = f"s{si}"
+    z = {k: z[k][:nf] for k in z.files if k.startswith(t + "_")}
     np.testing.assert_array_equal(np.packbits(out["u_hat"], axis=1), z[f"{t}_u_hat"])
     np.testing.assert_array_equal(out["prop"], z[f"{t}_prop"])
     np.testing.assert_array_equal(out["converged"], z[f"{t}_converged"])

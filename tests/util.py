@@ -10,7 +10,7 @@ from paper_2102_11089_b200 import configs
 from paper_2102_11089_b200.codes import build_tanner
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-FILES = {"c0": "C0", "c1": "C1", "c2": "C2", "c3": "C3"}
+FILES = {"c0": "C0", "c1": "C1", "c2": "C2", "c3": "C3", "c3b": "C3"}
 
 
 @functools.lru_cache(maxsize=None)
@@ -20,7 +20,7 @@ def load_code(key):
     return spec, build_tanner(spec.h)
 
 
-def golden_cases(files=("c0", "c1", "c2", "c3")):
+def golden_cases(files=("c0", "c1", "c2", "c3", "c3b")):
     out = []
     for f in files:
         z = np.load(GOLDEN / f"{f}.npz")
