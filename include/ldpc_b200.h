@@ -76,7 +76,21 @@ typedef struct {
                              3 all in shared memory, 4 per-edge + per-VN state in HBM (trees in smem) */
   int32_t want_trace;     /* 1: keep pre_total for every kind and allow ldpc_decode_traced outputs
                              (decode(..., want_trace=True), schedules.py:111-158) */
+  int32_t variant;        /* 0 = the tuned engine choice; else LDPC_VARIANT_* bits (tests and
+                             measurement: pin one engine so the alternatives can be compared) */
 } ldpc_sched_t;
+
+/* ldpc_sched_t.variant bits.  Flooding / layered engine (mask LDPC_VARIANT_FIXED_MASK): */
+#define LDPC_VARIANT_FIXED_PHASE 0x1   /* batch-wide phase kernels */
+#define LDPC_VARIANT_FIXED_TILE 0x2    /* one persistent CTA per 32-frame group */
+#define LDPC_VARIANT_FIXED_PIPE 0x3    /* the tile engine with cp.async staging */
+#define LDPC_VARIANT_FIXED_MASK 0x3
+#define LDPC_VARIANT_CHECK_TMA 0x4     /* phase engine: TMA bulk-copy check kernel */
+#define LDPC_VARIANT_CHECK_LEGACY 0x8  /* phase engine: load-wait-compute check kernel */
+#define LDPC_VARIANT_NO_LAYERED_SIGN 0x10 /* layered: separate VN pass for sign words */
+#define LDPC_VARIANT_LANES32 0x20      /* dynamic: 32 lanes per frame */
+#define LDPC_VARIANT_LANES16 0x40      /* dynamic: 16 lanes per frame (2 frames per warp) */
+#define LDPC_VARIANT_FULL_TREE 0x80    /* dynamic (debug): recompute every touched tree group */
 
 /* Build the device-resident Tanner graph (edge ids in (check, vn) order,
  * vn_edges = stable argsort of edge_vn).  Replaces build_tanner's arrays

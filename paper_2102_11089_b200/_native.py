@@ -23,7 +23,21 @@ class LdpcSched(C.Structure):
                 ("gamma", C.c_double), ("selection_seed", C.c_int64),
                 ("precision", C.c_int32), ("llr_f64", C.c_int32),
                 ("max_resident", C.c_int32), ("placement", C.c_int32),
-                ("want_trace", C.c_int32)]
+                ("want_trace", C.c_int32), ("variant", C.c_int32)]
+
+
+# ldpc_sched_t.variant bits (include/ldpc_b200.h)
+VARIANTS = {"fixed_phase": 0x1, "fixed_tile": 0x2, "fixed_pipe": 0x3, "check_tma": 0x4,
+            "check_legacy": 0x8, "no_layered_sign": 0x10, "lanes32": 0x20, "lanes16": 0x40,
+            "full_tree": 0x80}
+
+
+def variant_bits(names):
+    bits = 0
+    for n in (names.split(",") if isinstance(names, str) else names or ()):
+        if n:
+            bits |= VARIANTS[n]
+    return bits
 
 
 # every exported symbol of include/ldpc_b200.h

@@ -289,8 +289,7 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
   const long long sh[4] = {sE + sN + sT + sc, sN + sT + sc, sT + sc, sc};  // shared bytes per frame
   const long long hb[4] = {0, sE, sE + sN, sE + sN + sT};                 // HBM bytes per frame
   struct Cand { int mode, g16, wpb; long long smem; int occ; long long frames; };
-  const char* lanes_env = getenv("LDPC_LANES");
-  const int lanes_force = lanes_env ? atoi(lanes_env) : 0;
+  const int lanes_force = (s->variant & LDPC_VARIANT_LANES32) ? 32 : (s->variant & LDPC_VARIANT_LANES16) ? 16 : 0;
   auto make = [&](int mode, int g16) {
     Cand c{mode, g16, 0, 0, 0, 0};
     const int fpw = g16 ? 2 : 1;
@@ -417,11 +416,11 @@ int fixed_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, FixedPla
 // Engine choice for flooding / layered: "phase" (batch-wide phases, default),
 // "tile" (one persistent CTA per 32-frame group), "pipe" (tile + cp.async).
 int fixed_engine_choice(const ldpc_sched_t* s, long long B) {
-  const char* e = getenv("LDPC_FIXED_ENGINE");
-  if (e) {
-    if (!strcmp(e, "tile")) return 1;
-    if (!strcmp(e, "pipe")) return 2;
-    return 0;
+  switch (s->variant & LDPC_VARIANT_FIXED_MASK) {
+    case LDPC_VARIANT_FIXED_PHASE: return 0;
+    case LDPC_VARIANT_FIXED_TILE: return 1;
+    case LDPC_VARIANT_FIXED_PIPE: return 2;
+    default: break;
   }
   // float64 with many waves of 32-frame groups: the per-group persistent
   // kernel keeps each group's state L2-hot across iterations and has no tail
@@ -433,10 +432,10 @@ int fixed_engine_choice(const ldpc_sched_t* s, long long B) {
 
 // Phase engine: the TMA-fed strip kernels (fixed_tma.cuh) except float64
 // flooding, where the load-wait-compute kernel measured faster (C3: 27 vs 40 ms
-// per check launch); LDPC_PHASE_CHECK=legacy|tma overrides.
+// per check launch); LDPC_VARIANT_CHECK_TMA / _LEGACY override.
 bool phase_use_tma(const ldpc_sched_t* s) {
-  const char* pc = getenv("LDPC_PHASE_CHECK");
-  if (pc) return !!strcmp(pc, "legacy");
+  if (s->variant & LDPC_VARIANT_CHECK_TMA) return true;
+  if (s->variant & LDPC_VARIANT_CHECK_LEGACY) return false;
   return !(s->precision == LDPC_F64 && s->kind == KIND_FLOODING);
 }
 
@@ -475,26 +474,17 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
   const Tiling& tl = layered ? G->layer : G->flood;
   const Strips& sp = layered ? G->slayer : G->sflood;
   cudaFuncSetAttribute(K.check, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_check);
-  // check phase: the TMA-fed warp-specialised kernel unless LDPC_PHASE_CHECK=legacy
+  // check phase: the TMA-fed warp-specialised kernel unless LDPC_VARIANT_CHECK_LEGACY.
+  // Layered runs one check launch per dependency level.  (Round 1 also tried all
+  // levels in one launch ordered by per-group dependency counters: within 3 % --
+  // the check kernel's DRAM traffic, not the relaunches, bounds the sweep -- and
+  // it needs every CTA co-resident, so it was removed; fusing the flooding check
+  // and VN phases measured 1.5x slower: VN items stall on the slowest CTA.)
   const bool use_tma = phase_use_tma(s);
-  // layered: LDPC_LAYERED_FUSE=1 runs all levels in one check launch ordered by
-  // per-group dependency counters; measured within 3 % of one launch per level on
-  // C2/C3 (the check kernel's DRAM traffic, not the relaunches, bounds the sweep),
-  // and it relies on every CTA of the grid being co-resident, so off by default.
-  // (Fusing the flooding check and VN phases the same way, for L2 reuse of the
-  // fresh c2v rows, measured 1.5x slower: VN items stall on the slowest CTA.)
-  const char* fz = getenv("LDPC_LAYERED_FUSE");
-  const bool fuse_levels = fz && !strcmp(fz, "1");
-  const char* lw = getenv("LDPC_LAYERED_WINDOW");  // fused levels: groups per window (L2 reuse of totals)
-  const int lwin = lw ? atoi(lw) : 0;
-  const char* ad = getenv("LDPC_ALT_DIR");  // alternate group order per level (default on)
-  const bool alt_dir = !(ad && !strcmp(ad, "0"));
   // layered: sign words / error tallies from the check phase (every VN has an
-  // edge, so each VN's last-level commit sees its final total); LDPC_LAYERED_SIGN=0 off
-  const char* vr = getenv("LDPC_VN_REVERSE");  // flooding VN phase in reverse group order (opt-in)
-  const bool vn_rev = vr && !strcmp(vr, "1");
-  const char* ls = getenv("LDPC_LAYERED_SIGN");
-  const bool layered_sign = layered && use_tma && G->min_dv > 0 && !(ls && !strcmp(ls, "0"));
+  // edge, so each VN's last-level commit sees its final total);
+  // LDPC_VARIANT_NO_LAYERED_SIGN runs the separate VN pass instead
+  const bool layered_sign = layered && use_tma && G->min_dv > 0 && !(s->variant & LDPC_VARIANT_NO_LAYERED_SIGN);
   if (use_tma) {
     cudaFuncSetAttribute(K.check_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem);
     cudaFuncSetAttribute(K.vn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K.vn_smem);
@@ -537,8 +527,8 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     p.done = p.iters + pl.chunk * kFixedFrames;
     p.s_lvl = sp.lvl_sptr;
     p.layered_sign = layered_sign ? 1 : 0;
-    p.vn_reverse = vn_rev ? 1 : 0;
-    p.lwin = lwin;
+    p.vn_reverse = 0;
+    p.lwin = 0;
     p.level_tptr = tl.level_tptr;
     p.tile_eptr = tl.tile_eptr;
     p.te_list = tl.te_list;
@@ -578,22 +568,17 @@ int phase_decode(const ldpc_graph* G, const void* llr, long long B, const ldpc_s
     for (int it = 1; it <= I; ++it) {
       const std::vector<int>& lvl = use_tma ? sp.h_level_sptr : tl.h_level_tptr;
       const int nlev = (int)lvl.size() - 1;
-      if (use_tma && fuse_levels && nlev > 1) {
-        // all levels in one launch; per-group dependency counters keep the order
-        int L0 = 0, L1 = nlev, dep = (it - 1) * lvl[nlev], rev = 0;
-        void* ac[] = {&p, &L0, &L1, &dep, &rev};
-        if (int rc = launch(K.check_tma_fused, G_ * lvl[nlev], K.tma_smem, ac, K.tma_threads)) return rc;
-      } else {
+      {
         for (int L = 0; L < nlev; ++L) {
           int t_lo = lvl[L], t_hi = lvl[L + 1];
           if (t_hi <= t_lo) continue;
           if (use_tma) {
             // alternate the group order level to level: a level starts on the
             // groups the previous one ended with (their totals are L2-hot)
-            int L0 = L, L1 = L + 1, dep = -1, rev = (L & 1) && alt_dir ? 1 : 0;
+            int L0 = L, L1 = L + 1, dep = -1, rev = (L & 1) ? 1 : 0;
             void* ac[] = {&p, &L0, &L1, &dep, &rev};
             // layered: the FUSED build (spill-free allocation), one level per launch
-            void* fn = layered && !getenv("LDPC_TMA_CONSUMERS") ? K.check_tma_fused : K.check_tma;
+            void* fn = layered ? K.check_tma_fused : K.check_tma;
             if (int rc = launch(fn, G_ * (t_hi - t_lo), K.tma_smem, ac, K.tma_threads)) return rc;
           } else {
             void* ac[] = {&p, &t_lo, &t_hi};
@@ -632,6 +617,9 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
   if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
   if (s->want_trace != 0 && s->want_trace != 1) return LDPC_ERR_INVALID;
+  if (s->variant & ~0xff) return LDPC_ERR_INVALID;
+  if ((s->variant & LDPC_VARIANT_LANES32) && (s->variant & LDPC_VARIANT_LANES16)) return LDPC_ERR_INVALID;
+  if ((s->variant & LDPC_VARIANT_CHECK_TMA) && (s->variant & LDPC_VARIANT_CHECK_LEGACY)) return LDPC_ERR_INVALID;
   return LDPC_OK;
 }
 
@@ -698,7 +686,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.kt = kt;
     p.next = next;
     p.step_log = g_step_log;
-    p.dbg_full_tree = getenv("LDPC_DEBUG_FULL_TREE") ? 1 : 0;
+    p.dbg_full_tree = (s->variant & LDPC_VARIANT_FULL_TREE) ? 1 : 0;
     p.dump_step = g_dump_step;
     p.dump_buf = g_dump_buf;
     p.log_cap = g_log_cap;

@@ -78,17 +78,20 @@ class DecodeResult:
 
 
 class DeviceGraph:
-    """Device-resident Tanner graph handle (ldpc_graph_create)."""
+    """Device-resident Tanner graph handle (ldpc_graph_create) on one GPU."""
 
-    def __init__(self, g: TannerGraph):
+    def __init__(self, g: TannerGraph, device=None):
         L = _native.lib()
         arrs = [np.ascontiguousarray(a, dtype=np.int32)
                 for a in (g.edge_cn, g.edge_vn, g.cn_ptr, g.vn_ptr, g.vn_edges)]
         self._keep = arrs
+        self.device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
         h = C.c_void_p()
-        _native.check(L.ldpc_graph_create(*[a.ctypes.data_as(C.c_void_p) for a in arrs],
-                                          g.n_vars, g.n_checks, g.n_edges, C.byref(h)),
-                      "ldpc_graph_create")
+        with torch.cuda.device(self.device):  # the handle's arrays live on this device
+            _native.check(L.ldpc_graph_create(*[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                              g.n_vars, g.n_checks, g.n_edges, C.byref(h)),
+                          "ldpc_graph_create")
         self.handle = h
         info = np.zeros(7, np.int64)
         L.ldpc_graph_info(h, info.ctypes.data_as(C.c_void_p))
@@ -104,50 +107,64 @@ class DeviceGraph:
         except Exception:
             pass
 
-    def workspace(self, sched, B, device):
+    def workspace(self, sched, B, stream):
+        """Scratch for one decode, cached per stream: decodes on different
+        streams never share state, and a buffer is allocated on the stream
+        that uses it, so the caching allocator only recycles it after the
+        work queued there (the C ABI's stream-ordered contract)."""
         L = _native.lib()
         sz = C.c_size_t()
         _native.check(L.ldpc_workspace_size(self.handle, C.byref(sched), int(B), C.byref(sz)),
                       "ldpc_workspace_size")
-        key = (device, sz.value)
-        ws = self._ws.get(device)
+        key = stream.cuda_stream
+        ws = self._ws.get(key)
         if ws is None or ws.numel() < sz.value:
-            ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=device)
-            self._ws[device] = ws
+            self._ws.pop(key, None)
+            with torch.cuda.stream(stream):
+                ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
         return ws
 
 
-def device_graph(code_or_graph):
-    """Cached DeviceGraph for a CodeSpec / TannerGraph."""
+def _tanner_of(code: CodeSpec) -> TannerGraph:
+    """The TannerGraph of a CodeSpec, cached on the (frozen) object itself so
+    it lives exactly as long as the code does."""
+    g = code.__dict__.get("_b200_tanner")
+    if g is None:
+        g = build_tanner(code.h)
+        object.__setattr__(code, "_b200_tanner", g)
+    return g
+
+
+def device_graph(code_or_graph, device=None):
+    """Cached DeviceGraph of a CodeSpec / TannerGraph on `device` (default: current)."""
     g = code_or_graph
     if isinstance(g, CodeSpec):
-        cache = _code_cache.setdefault(id(g), {})
-        if "tanner" not in cache:
-            cache["tanner"] = build_tanner(g.h)
-            cache["spec"] = g
-        g = cache["tanner"]
-    dg = g._cache.get("device")
+        g = _tanner_of(g)
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    per_dev = g._cache.setdefault("device", {})
+    dg = per_dev.get(device.index)
     if dg is None:
-        dg = DeviceGraph(g)
-        g._cache["device"] = dg
+        dg = DeviceGraph(g, device)
+        per_dev[device.index] = dg
     return dg
-
-
-_code_cache = {}
 
 
 PLACEMENTS = {"auto": 0, "hbm": 1, "split": 2, "smem": 3, "trees": 4}
 
 
 def _sched(config: ScheduleConfig, k_info: int, llr_f64: bool, max_resident=0, placement="auto",
-           want_trace=False):
+           want_trace=False, variant=0):
     seed = int(config.selection_seed) & 0xFFFFFFFFFFFFFFFF
     if seed >= 1 << 63:
         seed -= 1 << 64
     return _native.LdpcSched(KIND_IDS[config.kind], KERNELS[config.kernel], config.i_max,
                              config.n_p, config.n_g, int(k_info), float(config.gamma), seed,
                              PRECISIONS[config.precision], 1 if llr_f64 else 0,
-                             int(max_resident), PLACEMENTS[placement], 1 if want_trace else 0)
+                             int(max_resident), PLACEMENTS[placement], 1 if want_trace else 0,
+                             _native.variant_bits(variant) if not isinstance(variant, int) else variant)
 
 
 def _ptr(t):
@@ -156,7 +173,7 @@ def _ptr(t):
 
 def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, device=None,
                  stream=None, out=None, max_resident=0, placement="auto", force_global=False,
-                 want_trace=False, gammas=None, j_counts=None):
+                 want_trace=False, gammas=None, j_counts=None, variant=0):
     """Decode a batch of frames on the GPU.
 
     code: CodeSpec (k_info taken from it) or TannerGraph (pass k_info).
@@ -166,7 +183,8 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
     [B, i_max+1] int32, kappa_hits_iter / kappa_trials_iter [B, i_max] int32.
     Asynchronous on the current (or given) stream.  placement (dynamic
     schedules): "auto", "smem", "split" (per-edge state in HBM/L2, per-VN
-    state in shared memory) or "hbm".
+    state in shared memory) or "hbm".  variant: engine pin for tests and
+    measurement (names of _native.VARIANTS, comma-separated; default: tuned).
     """
     if isinstance(code, CodeSpec):
         spec = code
@@ -175,8 +193,10 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
         spec = None
         if k_info is None:
             raise ValueError("k_info is required when decoding from a TannerGraph")
-    dg = device_graph(graph if graph is not None else code)
     device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    dg = device_graph(graph if graph is not None else code, device)
     if not torch.is_tensor(llrs):
         llrs = torch.from_numpy(np.ascontiguousarray(llrs))
     if llrs.dtype not in (torch.float32, torch.float64):
@@ -191,7 +211,14 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
     if force_global:
         placement = "hbm"
     tracing = bool(want_trace) or gammas is not None
-    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, placement, tracing)
+    sched = _sched(config, k_info, llrs.dtype == torch.float64, max_resident, placement, tracing, variant)
+    st = stream if stream is not None else torch.cuda.current_stream(device)
+    with torch.cuda.device(device), torch.cuda.stream(st):
+        return _decode_on(dg, llrs, B, I, sched, config, device, st, out, tracing, want_trace, gammas,
+                          j_counts)
+
+
+def _decode_on(dg, llrs, B, I, sched, config, device, st, out, tracing, want_trace, gammas, j_counts):
     if out is None:
         out = {
             "u_hat": torch.empty((B, dg.N), dtype=torch.int8, device=device),
@@ -203,8 +230,7 @@ def decode_batch(code, llrs, config: ScheduleConfig, graph=None, k_info=None, de
             "kappa_hits_iter": torch.zeros((B, max(I, 1)), dtype=torch.int32, device=device),
             "kappa_trials_iter": torch.zeros((B, max(I, 1)), dtype=torch.int32, device=device),
         }
-    ws = dg.workspace(sched, B, device)
-    st = stream if stream is not None else torch.cuda.current_stream(device)
+    ws = dg.workspace(sched, B, st)
     L = _native.lib()
     if not tracing:
         rc = L.ldpc_decode(dg.handle, _ptr(llrs), B, C.byref(sched), _ptr(out["u_hat"]), _ptr(out["prop"]),
@@ -249,11 +275,7 @@ def decode(code: CodeSpec, channel_llrs, config: ScheduleConfig, graph=None,
            want_trace=False) -> DecodeResult:
     """Run one frame through the configured schedule (schedules.py:111-158)."""
     if graph is None:
-        cache = _code_cache.setdefault(id(code), {})
-        if "tanner" not in cache:
-            cache["tanner"] = build_tanner(code.h)
-            cache["spec"] = code
-        graph = cache["tanner"]
+        graph = _tanner_of(code)
     chl = np.asarray(channel_llrs, dtype=np.float64)
     if chl.ndim != 1 or len(chl) != graph.n_vars:
         raise ValueError("channel LLR length mismatch")

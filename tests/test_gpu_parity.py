@@ -200,38 +200,26 @@ def test_device_frame_generation_statistics():
     assert abs(fd - fh) < 2.58 * np.sqrt(2 * fh * (1 - fh) / 20000) + 1e-3
 
 
-def _with_env(name, value, fn):
-    import os
-    old = os.environ.get(name)
-    os.environ[name] = value
-    try:
-        return fn()
-    finally:
-        if old is None:
-            del os.environ[name]
-        else:
-            os.environ[name] = old
-
-
 @pytest.mark.parametrize("code_key,eb,i_max,count", [("C0", 2.0, 5, 700), ("C2", 1.0, 3, 200), ("C3", 1.0, 2, 40)])
 @pytest.mark.parametrize("kernel", ["exact", "minsum"])
 def test_fixed_check_engines_match(code_key, eb, i_max, count, kernel):
-    """TMA-fed strip kernels (fixed_tma.cuh; layered: one launch per level, and
-    all levels in one launch ordered by per-group dependency counters) == the
-    load-wait-compute phase kernels == the per-group persistent kernel, bit for
-    bit in float64, flooding and layered (odd batch: a partial group)."""
+    """TMA-fed strip kernels (fixed_tma.cuh; layered: one launch per level) ==
+    the load-wait-compute phase kernels == the per-group persistent kernel ==
+    its cp.async pipeline build, bit for bit in float64, flooding and layered
+    (odd batch: a partial group).  Engines are pinned through
+    ldpc_sched_t.variant."""
     spec, g = load_code(code_key)
     llrs = llr_batch(spec, eb, seed=5, start=0, count=count)
     for kind in ("flooding", "layered"):
         cfg = _cfg({"kind": kind, "i_max": i_max, "kernel": kernel})
-        a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
-        b = _with_env("LDPC_PHASE_CHECK", "legacy", lambda: _gpu(spec, llrs, cfg))
-        c = _with_env("LDPC_FIXED_ENGINE", "tile", lambda: _gpu(spec, llrs, cfg))
-        d = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
+        a = _gpu(spec, llrs, cfg, variant="fixed_phase,check_tma")
+        b = _gpu(spec, llrs, cfg, variant="fixed_phase,check_legacy")
+        c = _gpu(spec, llrs, cfg, variant="fixed_tile")
+        d = _gpu(spec, llrs, cfg, variant="fixed_pipe")
         for k in FIELDS:
             np.testing.assert_array_equal(a[k], b[k], err_msg=f"{code_key} {kind} {kernel} {k}")
             np.testing.assert_array_equal(a[k], c[k], err_msg=f"{code_key} {kind} {kernel} {k} (tile engine)")
-            np.testing.assert_array_equal(a[k], d[k], err_msg=f"{code_key} {kind} {kernel} {k} (levels fused)")
+            np.testing.assert_array_equal(a[k], d[k], err_msg=f"{code_key} {kind} {kernel} {k} (pipe engine)")
 
 
 @pytest.mark.parametrize("kind", ["flooding", "layered"])
@@ -268,17 +256,15 @@ def test_fixed_fp32_statistics(kind):
 
 @pytest.mark.parametrize("count", [1, 33])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_layered_fused_levels_small_batches(count, precision):
-    """One or two 32-frame groups: every level's items depend on the items just
-    before them (the case the dependency counters must not deadlock on)."""
+def test_layered_small_batches_sign_pass(count, precision):
+    """One or two 32-frame groups: sign words and error tallies formed in the
+    layered check phase == the separate VN pass."""
     spec, g = load_code("C2")
     llrs = llr_batch(spec, 1.0, seed=9, start=0, count=count)
     cfg = _cfg({"kind": "layered", "i_max": 4, "precision": precision})
-    a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
-    b = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
-    c = _with_env("LDPC_LAYERED_SIGN", "0", lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg)))
+    a = _gpu(spec, llrs, cfg, variant="fixed_phase,check_tma")
+    c = _gpu(spec, llrs, cfg, variant="fixed_phase,check_tma,no_layered_sign")
     for k in FIELDS:
-        np.testing.assert_array_equal(a[k], b[k])
         np.testing.assert_array_equal(a[k], c[k], err_msg=f"{k}: sign pass in the check phase vs separate VN pass")
 
 
@@ -312,18 +298,3 @@ def test_fp32_messages_within_1e4_first_1000_updates(kind):
                                      err_msg=f"{kind} frame {f}")
         compared += n
     assert compared >= 0.8 * 64 * 1000, (compared, diverged)
-
-
-@pytest.mark.parametrize("window", [1, 2, 3])
-@pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_layered_fused_levels_group_windows(window, precision):
-    """Levels fused, items ordered in windows of `window` groups (level-major
-    inside a window): same answers as one launch per level."""
-    spec, g = load_code("C2")
-    llrs = llr_batch(spec, 1.0, seed=4, start=0, count=200)
-    cfg = _cfg({"kind": "layered", "i_max": 3, "precision": precision})
-    a = _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))
-    b = _with_env("LDPC_LAYERED_FUSE", "1", lambda: _with_env(
-        "LDPC_LAYERED_WINDOW", str(window), lambda: _with_env("LDPC_PHASE_CHECK", "tma", lambda: _gpu(spec, llrs, cfg))))
-    for k in FIELDS:
-        np.testing.assert_array_equal(a[k], b[k])

@@ -1,4 +1,4 @@
-"""Time flooding / layered under each fixed engine (LDPC_FIXED_ENGINE = phase |
+"""Time flooding / layered under each fixed engine (ldpc_sched_t.variant = phase |
 tile | pipe) on the bench codes, to set the engine-choice heuristic.
 
     python tools/fixed_engines.py [C0,C1,C2,C3] [f64,f32] [phase,tile,pipe] [tag]
@@ -31,15 +31,15 @@ for key in codes:
         for kind in ("flooding", "layered"):
             cfg = ScheduleConfig(kind=kind, i_max=imax, precision=prec)
             for eng in engines:
-                os.environ["LDPC_FIXED_ENGINE"] = eng
+                var = {"phase": "fixed_phase", "tile": "fixed_tile", "pipe": "fixed_pipe"}[eng]
                 out = None
                 for _ in range(2):
-                    out = decode_batch(g, llr, cfg, k_info=spec.k_info, out=out)
+                    out = decode_batch(g, llr, cfg, k_info=spec.k_info, out=out, variant=var)
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
                 for _ in range(3):
-                    out = decode_batch(g, llr, cfg, k_info=spec.k_info, out=out)
+                    out = decode_batch(g, llr, cfg, k_info=spec.k_info, out=out, variant=var)
                 b.record()
                 torch.cuda.synchronize()
                 ms = a.elapsed_time(b) / 3
