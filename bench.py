@@ -1,18 +1,24 @@
 """Benchmark: decoded frames/s and C2V edge updates/s per schedule (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C0|C1|C2|C3|C4|C3F]
 
-Workload (default): BASELINE.json configs[1] -- the WiFi-shaped n=648 QC code
-(Z=27), BPSK-AWGN at Eb/N0 = 2.0 dB (mid-sweep), i_max = 3, batch 100,000
-frames, and every schedule the config names (flooding, layered, RBP, CIRBP,
-LMDRBP, sLMDRBP, LMD-CIRBP, ME-CIRBP M=4, ME-RBP M=4).  One step = the batch
-decoded once by every schedule.  value = total C2V edge updates / time over
-the K timed steps (whole job, all ranks).  The batch's LLRs (259 MB) exceed
-the 126 MB L2, so every step streams its inputs from HBM.
+Workload (default): BASELINE.json configs[3] -- the largest single-GPU config,
+the BG1-shaped n=26112 QC code (Z=384, 2Z punctured), BPSK-AWGN at Eb/N0 =
+1.0 dB, budget i_max = 10 (10 E C2V updates), batch 10,000 frames, float64
+(the reference's arithmetic), schedules flooding, layered, RBP, CIRBP and
+ME-CIRBP M=64.  One step = the batch decoded once by every schedule.  value =
+total C2V edge updates / time over the K timed steps (whole job, all ranks).
+The batch's LLRs (1.04 GB) exceed the 126 MB L2, so every step streams its
+inputs from HBM.  The C1 workload (configs[1], every schedule, 100k frames)
+is measured in the same run as a secondary block (`secondary`, 2 steps).
 
---impl reference: the reference's decode algorithm on the host cores (the C
-oracle port, oracle/ldpc_oracle.c, all threads), same config/metric, each step
-a bounded seeded sample of the batch.
+--impl reference: the reference's OWN decoder (ldpc_ids.schedules.decode,
+numba, installed unmodified in baseline/_ref) on all host cores through the
+reference harness's process-pool pattern (sim.py:233-259), same config and
+metric, each step a bounded seeded sample of the batch (one frame per core);
+layered (absent from the reference) runs on the C port (oracle/ldpc_oracle.c).
+Without baseline/_ref the C port runs every schedule.
 """
 
 from __future__ import annotations
@@ -41,6 +47,8 @@ WORKLOADS = {
                                    ("me_cirbp", 4), ("me_cirbp", 16)]),
     "C3": ("C3", 1.0, 10, 10_000, [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1),
                                    ("me_cirbp", 64)]),
+    "C3b": ("C3", 0.5, 10, 10_000, [("flooding", 1), ("layered", 1), ("rbp", 1), ("cirbp", 1),
+                                    ("me_cirbp", 64)]),
     # C4 = the C2 code at 0 dB, budget 20 E (batch/occupancy sweep: --batch)
     "C4": ("C2", 0.0, 20, 16_384, [("me_cirbp", 1), ("me_cirbp", 4), ("me_cirbp", 16), ("me_cirbp", 64),
                                    ("rbp", 1)]),
@@ -129,58 +137,79 @@ def make_inputs(spec, ebn0, start, count):
     return llr_batch(spec, ebn0, seed=0, start=start, count=count, dtype=np.float32)
 
 
+def _sname(kind, n_p):
+    return kind + (f"/M{n_p}" if kind.startswith("me_") else "")
+
+
 def run_reference(args, wl):
-    """Reference algorithm (oracle port) on all host cores; rank 0 only."""
+    """The reference's own decoder on all host cores; rank 0 only (the other
+    ranks exit without work)."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    from oracle import pyoracle
+    from oracle import pyoracle, refpool
     from paper_2102_11089_b200 import configs
     from paper_2102_11089_b200.codes import build_tanner
     key, ebn0, i_max, batch, scheds = wl
     spec = getattr(configs, f"make_{key.lower()}_code")()
     g = build_tanner(spec.h)
     cores = os.cpu_count() or 1
-    sample = args.ref_sample or max(64, min(4096, 2 * cores * 64))
+    sample = args.ref_sample or cores
     llr = make_inputs(spec, ebn0, 0, sample).astype(np.float64)
+    use_ref = refpool.available() and not args.ref_port
+    pool = refpool.RefPool(spec, scheds, i_max, workers=cores) if use_ref else None
+    ref_kinds = set(pool.scheds) if pool else set()
+    port = [(k, n) for k, n in scheds if (k, n) not in ref_kinds]
+
     def step():
-        upd = frames = 0
         t0 = time.perf_counter()
-        for kind, n_p in scheds:
-            r = pyoracle.decode_batch(g, llr, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
-                                      threads=cores)
+        upd = 0
+        if pool:
+            r, _ = pool.run(llr)
+            upd += sum(v[0] for v in r.values())
+        for kind, n_p in port:
+            r = pyoracle.decode_batch(g, llr, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p, threads=cores)
             upd += int(r["prop"].sum())
-            frames += len(llr)
-        return upd, frames, time.perf_counter() - t0
+        return upd, time.perf_counter() - t0
+
     for _ in range(args.warmup):
         step()
-    tot_u = tot_f = tot_t = 0
+    tot_u = tot_t = 0
     for _ in range(args.steps):
-        u, f, t = step()
+        u, t = step()
         tot_u += u
-        tot_f += f
         tot_t += t
+    if pool:
+        pool.close()
     val = tot_u / tot_t
+    what = ("ldpc_ids.schedules.decode (numba, baseline/_ref) over a %d-process pool (sim.py:233-259)"
+            % cores if pool else "C port oracle/ldpc_oracle.c, %d threads" % cores)
+    if pool and port:
+        what += "; " + ", ".join(_sname(k, n) for k, n in port) + " (not in the reference) on the C port"
     line = {
         "impl": "reference", "metric": f"C2V edge updates/s (all {args.workload} schedules); decoded frames/s",
         "value": val, "unit": "C2V edge updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "frames_per_s": tot_f / tot_t,
-        "config": {"workload": f"{args.workload} ({spec.label}): " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+        "frames_per_s": sample * len(scheds) * args.steps / tot_t,
+        "config": {"workload": f"{args.workload} ({spec.label}): " + ", ".join(_sname(k, n) for k, n in scheds),
                    "code": spec.label, "ebn0_db": ebn0, "i_max": i_max, "batch": sample},
-        "cpu_baseline": {"value": val, "unit": "C2V edge updates/s", "cores": cores, "kind": "port",
-                         "sample": f"first {sample} frames of the seeded batch, every schedule"},
+        "cpu_baseline": {"value": val, "unit": "C2V edge updates/s", "cores": cores,
+                         "kind": "reference" if pool else "port",
+                         "sample": f"first {sample} frames of the seeded batch per step, every schedule: {what}"},
         "e2e": {"value": val, "unit": "C2V edge updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
-    """Oracle on a bounded sample of the same batch, all host cores (rank 0, N=1
-    only): first one frame per core through every schedule, then, if that took
-    less than the budget, a larger sample scaled to ~budget_s."""
+def cpu_baseline(wl, spec, g, llr_host, gpu_outs, budget_s=20.0):
+    """C port (oracle/ldpc_oracle.c) on a bounded sample of the same batch, all
+    host cores (rank 0, N=1 only): first one frame per core through every
+    schedule, then, if that took less than the budget, a larger sample scaled
+    to ~budget_s.  Also reports, per schedule, the fraction of sample frames on
+    which the GPU's decode of the same frames (gpu_outs) is identical to the
+    oracle's (hard decisions and update count)."""
     from oracle import pyoracle
     key, ebn0, i_max, batch, scheds = wl
     cores = os.cpu_count() or 1
@@ -188,14 +217,21 @@ def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
     def run(sample):
         per, tot_u = {}, 0
         t0 = time.perf_counter()
-        for kind, n_p in scheds:
+        for si, (kind, n_p) in enumerate(scheds):
             t1 = time.perf_counter()
             r = pyoracle.decode_batch(g, sample, kind, i_max=i_max, k_info=spec.k_info, n_p=n_p,
                                       threads=cores)
             u = int(r["prop"].sum())
-            name = f"{kind}" + (f"/M{n_p}" if kind.startswith("me_") else "")
-            per[name] = {"updates_per_s": u / (time.perf_counter() - t1),
-                         "frame_errors": int((r["bit_errors_at"][:, -1] > 0).sum()), "frames": len(sample)}
+            n = len(sample)
+            gu = gpu_outs[si]["u_hat"][:n].cpu().numpy()
+            gp = gpu_outs[si]["prop"][:n].cpu().numpy()
+            same = (gu == r["u_hat"]).all(1) & (gp == r["prop"])
+            per[_sname(kind, n_p)] = {"updates_per_s": u / (time.perf_counter() - t1),
+                                      "frame_errors": int((r["bit_errors_at"][:, -1] > 0).sum()),
+                                      "bit_errors": int(r["info_bit_errors_at"][:, -1].sum()),
+                                      "bits_mean": float(r["info_bit_errors_at"][:, -1].mean()),
+                                      "bits_sd": float(r["info_bit_errors_at"][:, -1].std(ddof=1)) if n > 1 else 0.0,
+                                      "frames": n, "identical": int(same.sum())}
             tot_u += u
         return tot_u, time.perf_counter() - t0, per
 
@@ -208,7 +244,35 @@ def cpu_baseline(wl, spec, g, llr_host, budget_s=20.0):
             "sample": f"first {n} frames of the batch through every schedule ({t:.1f} s)",
             "frames_per_s": n * len(scheds) / t,
             "per_schedule_updates_per_s": {k: v["updates_per_s"] for k, v in per.items()},
-            "per_schedule_fer": {k: (v["frame_errors"], v["frames"]) for k, v in per.items()}}
+            "per_schedule_fer": {k: (v["frame_errors"], v["frames"]) for k, v in per.items()},
+            "per_schedule_info_bits": {k: (v["bits_mean"], v["bits_sd"], v["frames"]) for k, v in per.items()},
+            "gpu_oracle_identical": {k: [v["identical"], v["frames"]] for k, v in per.items()}}
+
+
+def cpu_reference(wl, spec, llr_host, budget_s=30.0):
+    """The reference's own numba decoder (baseline/_ref) over the harness's
+    process pool on the first frames of the batch: the `--impl reference` leg,
+    reported beside the C port (rank 0, N=1 only)."""
+    from oracle import refpool
+    if not refpool.available():
+        return None
+    key, ebn0, i_max, batch, scheds = wl
+    cores = os.cpu_count() or 1
+    pool = refpool.RefPool(spec, scheds, i_max, workers=cores)
+    try:
+        n = cores
+        r, t = pool.run(llr_host[:n])
+        if t < budget_s / 2:
+            n = int(min(len(llr_host), max(n, n * budget_s / max(t, 1e-3)) // cores * cores))
+            r, t = pool.run(llr_host[:n])
+    finally:
+        pool.close()
+    u = sum(v[0] for v in r.values())
+    return {"value": u / t, "unit": "C2V edge updates/s", "cores": cores, "kind": "reference",
+            "sample": f"first {n} frames, schedules {', '.join(_sname(k, m) for k, m in r)} through "
+                      f"ldpc_ids.schedules.decode (numba) on a {cores}-process pool ({t:.1f} s)",
+            "per_schedule_updates_per_s": {_sname(k, m): v[0] / t * len(r) for (k, m), v in r.items()},
+            "per_schedule_fer": {_sname(k, m): (v[1], n) for (k, m), v in r.items()}}
 
 
 def clopper_pearson(k, n, alpha=0.05):
@@ -220,16 +284,34 @@ def clopper_pearson(k, n, alpha=0.05):
 
 
 def run_ours(args, wl):
+    rank, world, local = dist_setup(args)
+    line = measure(args, wl, args.workload, args.steps, args.warmup, rank, world, local,
+                   batch=args.batch, cpu=rank == 0 and world == 1 and not args.no_cpu_baseline)
+    if args.workload == "C3" and not args.no_secondary and not args.only:
+        # BASELINE configs[1] (C1, every schedule) on the same clock, 2 timed steps
+        sec = measure(args, WORKLOADS["C1"], "C1", 2, 3, rank, world, local, batch=0, cpu=False)
+        line["secondary"] = {"C1": {k: sec[k] for k in ("metric", "value", "unit", "steps", "warmup",
+                                                         "ms_per_step", "dtype", "config", "e2e",
+                                                         "gpu_launches", "roofline")},
+                             "C1_per_schedule": {k: {q: v[q] for q in ("ms", "edge_updates_per_s", "frames_per_s",
+                                                                        "fer")}
+                                                 for k, v in sec["per_schedule"].items()}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=False):
     import torch
     from paper_2102_11089_b200 import configs
     from paper_2102_11089_b200 import dist as D
     from paper_2102_11089_b200.codes import build_tanner
     from paper_2102_11089_b200.schedules import ScheduleConfig, decode_batch, device_graph
 
-    rank, world, local = dist_setup(args)
-    key, ebn0, i_max, batch, scheds = wl
-    if args.batch:
-        batch = args.batch
+    key, ebn0, i_max, wl_batch, scheds = wl
+    batch = batch or wl_batch
     if args.only:
         scheds = [s for s in scheds if s[0] + (f"/M{s[1]}" if s[0].startswith("me_") else "") == args.only]
         if not scheds:
@@ -253,7 +335,7 @@ def run_ours(args, wl):
         return outs[idx]["_launches"]
 
     # warm-up (also yields the per-schedule work, identical every step)
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         for i, c in enumerate(cfgs):
             one(c, i, llr_dev)
     torch.cuda.synchronize()
@@ -261,8 +343,9 @@ def run_ours(args, wl):
     for i, c in enumerate(cfgs):
         cnt = outs[i]["counters"].cpu().numpy()
         fer = float((outs[i]["bit_errors_at"][:, -1] > 0).float().mean().item())
+        ber = float(outs[i]["info_bit_errors_at"][:, -1].double().sum().item()) / (batch * max(1, spec.k_info))
         work.append({"updates": int(cnt[:, 0].sum()), "bpu": bytes_per_update(c.kind, cnt, E, N, elem),
-                     "fer": fer, "counters": cnt.sum(0)})
+                     "fer": fer, "ber": ber, "counters": cnt.sum(0)})
 
     # timed region: device-resident inputs
     if world > 1:
@@ -271,12 +354,12 @@ def run_ours(args, wl):
     clocks = ClockSampler(local)
     clocks.start()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in cfgs] for _ in range(args.steps)]
+           for _ in cfgs] for _ in range(steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     launches = 0
     t_start.record(stream)
-    for s in range(args.steps):
+    for s in range(steps):
         for i, c in enumerate(cfgs):
             ev[s][i][0].record(stream)
             launches += one(c, i, llr_dev)
@@ -285,7 +368,7 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
-    sched_ms = [sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps)) / args.steps
+    sched_ms = [sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(steps)) / steps
                 for i in range(len(cfgs))]
 
     # e2e: pinned host LLRs in, host results out, through the public API
@@ -295,7 +378,7 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     e_start.record(stream)
     h2d = d2h = 0
-    for s in range(args.steps):
+    for s in range(steps):
         src = llr_pinned.to(dev, non_blocking=True)
         h2d += llr_pinned.numel() * llr_pinned.element_size()
         for i, c in enumerate(cfgs):
@@ -309,7 +392,7 @@ def run_ours(args, wl):
 
     step_updates = int(D.all_sum([sum(w["updates"] for w in work)])[0])  # all ranks
     t_max, e_max = (float(x) for x in D.all_max([total_ms, e2e_ms]))
-    job_updates = step_updates * args.steps
+    job_updates = step_updates * steps
     value = job_updates / (t_max / 1e3)
     e2e_value = job_updates / (e_max / 1e3)
 
@@ -332,16 +415,16 @@ def run_ours(args, wl):
     for i, (c, wk) in enumerate(zip(cfgs, work)):
         nm = c.kind + (f"/M{c.n_p}" if c.kind.startswith("me_") else "")
         per[nm] = {"ms": round(sched_ms[i], 3), "edge_updates_per_s": wk["updates"] / (sched_ms[i] / 1e3),
-                   "frames_per_s": batch / (sched_ms[i] / 1e3), "fer": wk["fer"],
+                   "frames_per_s": batch / (sched_ms[i] / 1e3), "fer": wk["fer"], "ber_info": wk["ber"],
                    "updates_per_frame": wk["updates"] / batch, "state_bytes_per_update": round(wk["bpu"], 1),
                    "state_GBps": wk["updates"] * wk["bpu"] / (sched_ms[i] / 1e3) / 1e9}
     line = {
-        "metric": f"C2V edge updates/s (all {args.workload} schedules); decoded frames/s",
-        "value": value, "unit": "C2V edge updates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "metric": f"C2V edge updates/s (all {wname} schedules); decoded frames/s",
+        "value": value, "unit": "C2V edge updates/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": t_max / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "frames_per_s": batch * len(cfgs) * args.steps * world / (t_max / 1e3),
-        "config": {"workload": f"{args.workload} ({spec.label}): " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
+        "frames_per_s": batch * len(cfgs) * steps * world / (t_max / 1e3),
+        "config": {"workload": f"{wname} ({spec.label}): " + ", ".join(f"{k}(n_p={n})" for k, n in scheds),
                    "code": spec.label, "N": N, "E": E, "ebn0_db": ebn0, "i_max": i_max,
                    "batch_per_gpu": batch, "l2": "inputs > L2 (batch LLRs %.0f MB)" % (llr_pinned.numel() * 4 / 1e6),
                    "parallelism": f"frames sharded over {world} GPU(s)"},
@@ -353,14 +436,20 @@ def run_ours(args, wl):
                              "formula in %s units x the launch's C2V updates) / the launch's CUDA-event "
                              "time; the dynamic schedules are a serial update chain per frame "
                              "(latency-bound), so this fraction is low by construction" % args.precision},
-        "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // args.steps,
-                "d2h_bytes_per_step": d2h // args.steps},
+        "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // steps,
+                "d2h_bytes_per_step": d2h // steps},
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(wl, spec, g, llr_host, budget_s=args.cpu_budget)
+    if cpu:
+        cb = cpu_baseline(wl, spec, g, llr_host, [outs[i] for i in range(len(cfgs))], budget_s=args.cpu_budget)
         line["cpu_baseline"] = cb
+        for nm, (same, n) in cb["gpu_oracle_identical"].items():
+            if nm in per:
+                per[nm]["gpu_oracle_identical"] = [same, n]
+        cr = cpu_reference(wl, spec, llr_host, budget_s=args.cpu_budget)
+        if cr:
+            line["cpu_reference"] = cr
         # FER vs oracle: the GPU's FER over the whole batch must lie inside the
         # oracle sample's 95 % Clopper-Pearson interval (north star)
         for nm, (k, n) in cb["per_schedule_fer"].items():
@@ -369,11 +458,16 @@ def run_ours(args, wl):
                 per[nm]["oracle_fer_sample"] = k / n
                 per[nm]["oracle_fer_ci95"] = [lo, hi]
                 per[nm]["fer_inside_oracle_ci95"] = bool(lo <= per[nm]["fer"] <= hi)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        # BER (info bits): normal CI over the sample's per-frame bit-error counts
+        for nm, (bits_mean, bits_sd, n) in cb["per_schedule_info_bits"].items():
+            if nm in per:
+                k = max(1, spec.k_info)
+                half = 1.96 * bits_sd / max(1, n) ** 0.5
+                lo, hi = max(0.0, (bits_mean - half) / k), (bits_mean + half) / k
+                per[nm]["oracle_ber_sample"] = bits_mean / k
+                per[nm]["oracle_ber_ci95"] = [lo, hi]
+                per[nm]["ber_inside_oracle_ci95"] = bool(lo <= per[nm]["ber_info"] <= hi)
+    return line
 
 
 def main():
@@ -382,12 +476,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C1", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--ref-port", action="store_true", help="reference arm on the C port even if baseline/_ref exists")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C1 block of the default C3 run")
     ap.add_argument("--only", default="", help="run one schedule of the workload (e.g. cirbp, me_rbp/M4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT"):

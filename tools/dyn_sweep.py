@@ -25,6 +25,7 @@ B = int(sys.argv[3]) if len(sys.argv) > 3 else 100_000
 prec = sys.argv[4] if len(sys.argv) > 4 else "f64"
 PLACES = sys.argv[5].split(",") if len(sys.argv) > 5 else ["auto", "split", "trees", "hbm"]
 FRACS = [float(x) for x in sys.argv[6].split(",")] if len(sys.argv) > 6 else [0, 0.25, 0.5, 0.75]
+VARIANTS = sys.argv[7].split(",") if len(sys.argv) > 7 else [""]
 eb, imax = EB[key]
 spec = getattr(configs, f"make_{'c2' if key == 'C4' else key.lower()}_code")()
 g = build_tanner(spec.h)
@@ -46,15 +47,15 @@ def timed(cfg, **kw):
 for ks in kinds:
     kind, _, m = ks.partition("/")
     cfg = ScheduleConfig(kind=kind, i_max=imax, n_p=int(m or 1), precision=prec)
-    for pl in PLACES:
+    for pl, var in [(a, b) for a in PLACES for b in VARIANTS]:
         for frac in FRACS:
             res = 0
             if frac:
                 res = max(32, int(frac * min(B, 148 * 64)))
             try:
-                ms, upd = timed(cfg, placement=pl, max_resident=res)
+                ms, upd = timed(cfg, placement=pl, max_resident=res, variant=var)
             except Exception as e:  # unsupported placement for this kind/code
                 print(json.dumps({"kind": ks, "placement": pl, "res": res, "error": str(e)[:80]}), flush=True)
                 break
-            print(json.dumps({"lib": os.environ.get("LDPC_B200_LIB", "default")[-12:], "code": key, "kind": ks, "placement": pl, "res": res, "ms": round(ms, 2),
+            print(json.dumps({"lib": os.environ.get("LDPC_B200_LIB", "default")[-12:], "code": key, "kind": ks, "placement": pl, "variant": var, "res": res, "ms": round(ms, 2),
                               "upd_per_s": upd / ms * 1e3}), flush=True)
