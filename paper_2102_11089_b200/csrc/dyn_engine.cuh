@@ -49,6 +49,20 @@ constexpr int dyn_min_blocks(int kind, bool f64) {
 
 constexpr int kFlatCiMax = 128;  // CIRBP: flat CI argmax when N <= this (else incremental tree)
 
+// max-tree storage (see "max trees" below)
+template <typename Key>
+struct alignas(2 * sizeof(Key)) L1Node {
+  Key k;
+  int i;
+};
+
+template <typename Key>
+struct TreeRef {
+  L1Node<Key>* l1;  // level 1
+  Key* up;          // levels >= 2: level l at up + geo.off[l] - geo.off[2]
+};
+
+
 struct DynParams {
   DevGraph g;
   int kind, kernel, i_max, n_p, n_g, k_info;
@@ -77,11 +91,12 @@ struct DynParams {
   long long slotE_bytes, slotN_bytes, slotT_bytes;
   long long o_c2v, o_pre, o_in, o_res;                           // E part
   long long o_total, o_pretot, o_ci, o_p0t, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
-  long long o_rtree, o_ridx, o_ctree, o_cidx;                    // T part
+  long long o_rl1, o_cl1;                                        // T part: level-1 tree nodes
+  long long slotU_bytes, o_rup, o_cup;                           // U part (shared memory): tree levels >= 2
   TreeGeom rgeo, cgeo;
   int flat_ci;            // CIRBP: flat CI argmax instead of a tree
   int scratch_bytes;      // per-warp shared scratch
-  int so_items, so_stage, so_nk, so_dl0, so_dl1, so_sizes, so_hist;
+  int so_items, so_stage, so_nk, so_opre, so_cj, so_ck, so_dl0, so_dl1, so_sizes, so_hist;
   int fast_sel;           // ME kinds with n_g <= 255: maintained groups + histogram
   // want_trace (E:192-217): pre_total upkeep for every kind, per-boundary rows
   // and fused J(gamma) counts (sim.py:172-183)
@@ -93,9 +108,8 @@ template <typename T, int G>
 struct Ctx {
   using Key = typename Num<T>::Key;
   Grp<G> w;            // this frame's lane group
-  T *c2v, *pre, *in, *res, *total, *pretot, *ci, *p0t, *tmp;  // p0t = p0(total), CI kinds
-  Key *rtree, *ctree;  // tree node keys, all levels
-  int *ridx, *cidx;    // level-1 argmax leaf of each 32-leaf group
+  T *c2v, *pre, *in, *res, *total, *pretot, *ci, *p0t, *tmp;  // p0t = p0_cache(total), CI kinds
+  TreeRef<Key> rt, ct;  // residual tree over E, CI tree over N
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
   uint8_t* gid;   // ME kinds: Alg.-4 group of each VN (maintained)
   int* hist;      // ME kinds: VNs per group (maintained)
@@ -105,6 +119,10 @@ struct Ctx {
   int4* items_buf;    // per-warp scratch for items built on the fly
   T* stage;       // staged check inputs of the last update
   Key* nk;        // new residual key of each item
+  T* cg;          // C2V of each item, staged with its inputs (aliases nk: read before nk is written)
+  T* opre;        // old pre of each item (pre_total upkeep)
+  int* cj;        // VN of each item (pre_total upkeep; -1: not its last occurrence)
+  Key* ck;        // CI key of each item's VN after the refresh (CI tree)
   int *dl0, *dl1; // dirty-node lists for tree maintenance
   int* sizes;     // Alg.4 group histogram
   long long cnt[kCounters];
@@ -125,28 +143,40 @@ __device__ __forceinline__ typename Num<T>::Key res_key(const Ctx<T, G>& c, int 
 }
 
 // ------------------------------------------------------------- max trees
-// Node keys for levels 1..L (tree + off[l]); level 1 also stores the index of
-// its maximal leaf (lowest index among equal keys), so an argmax descent ends
-// in shared memory without touching the leaves.  LeafFn: int -> Key.
+// Level-1 nodes (one per 32 leaves) hold the group's max key AND its argmax
+// leaf (lowest index among equal keys) in one record, so the last step of an
+// argmax descent is one load; they live in the frame's tree part (shared
+// memory or HBM by placement).  Levels >= 2 (E/1024 keys and fewer: 123 keys
+// for a BG1-sized code) always live in shared memory, so a descent or an
+// ancestor fix touches HBM at most once.  LeafFn: int -> Key.
+
+__host__ __device__ __forceinline__ int up_off(const TreeGeom& geo, int l) { return geo.off[l] - geo.off[2]; }
 
 template <typename Key, typename LeafFn>
-__device__ __forceinline__ Key child_key(const Key* tree, const TreeGeom& geo, int level, int child,
+__device__ __forceinline__ Key child_key(const TreeRef<Key>& t, const TreeGeom& geo, int level, int child,
                                          LeafFn leaf) {
   if (child >= geo.size[level]) return Key(0);
   if (level == 0) return leaf(child);
-  return tree[geo.off[level] + child];
+  if (level == 1) return t.l1[child].k;
+  return t.up[up_off(geo, level) + child];
+}
+
+template <typename Key>
+__device__ __forceinline__ void set_node(const TreeRef<Key>& t, const TreeGeom& geo, int level, int q, Key k) {
+  if (level == 1) t.l1[q].k = k;
+  else t.up[up_off(geo, level) + q] = k;
 }
 
 // lane-local scan of node q's 32 children (level l-1), strided by the group
 // width; returns the lane's (max key, lowest child index among ties)
 template <int G, typename Key, typename LeafFn>
-__device__ __forceinline__ Key child_scan(const Key* tree, const TreeGeom& geo, int l, int q, int lane,
+__device__ __forceinline__ Key child_scan(const TreeRef<Key>& t, const TreeGeom& geo, int l, int q, int lane,
                                           LeafFn leaf, int* bi) {
   Key m = 0;
   int b = 0x7fffffff;
 #pragma unroll
   for (int c = lane; c < 32; c += G) {
-    const Key k = child_key(tree, geo, l - 1, q * 32 + c, leaf);
+    const Key k = child_key(t, geo, l - 1, q * 32 + c, leaf);
     if (k > m || b == 0x7fffffff) { m = k; b = q * 32 + c; }
   }
   *bi = b;
@@ -154,26 +184,26 @@ __device__ __forceinline__ Key child_scan(const Key* tree, const TreeGeom& geo, 
 }
 
 template <int G, typename Key, typename LeafFn>
-__device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, const Grp<G>& w, LeafFn leaf) {
+__device__ void tree_build(const TreeRef<Key>& t, const TreeGeom& geo, const Grp<G>& w, LeafFn leaf) {
   for (int q = w.lane; q < geo.size[1]; q += G) {
     Key m = 0;
     int bi = q * 32;
     for (int c = 0; c < 32; ++c) {
-      Key k = child_key(tree, geo, 0, q * 32 + c, leaf);
+      Key k = child_key(t, geo, 0, q * 32 + c, leaf);
       if (k > m) { m = k; bi = q * 32 + c; }
     }
-    tree[geo.off[1] + q] = m;
-    idx1[q] = bi;
+    t.l1[q].k = m;
+    t.l1[q].i = bi;
   }
   w.sync();
   for (int l = 2; l <= geo.levels; ++l) {
     for (int q = w.lane; q < geo.size[l]; q += G) {
       Key m = 0;
       for (int c = 0; c < 32; ++c) {
-        Key k = child_key(tree, geo, l - 1, q * 32 + c, leaf);
+        Key k = child_key(t, geo, l - 1, q * 32 + c, leaf);
         m = k > m ? k : m;
       }
-      tree[geo.off[l] + q] = m;
+      t.up[up_off(geo, l) + q] = m;
     }
     w.sync();
   }
@@ -181,22 +211,57 @@ __device__ void tree_build(Key* tree, int* idx1, const TreeGeom& geo, const Grp<
 
 // Full recompute of level-1 group q from its leaves (group-cooperative).
 template <int G, typename Key, typename LeafFn>
-__device__ __forceinline__ void group_recompute(Key* tree, int* idx1, const TreeGeom& geo, int q,
+__device__ __forceinline__ void group_recompute(const TreeRef<Key>& t, const TreeGeom& geo, int q,
                                                 const Grp<G>& w, LeafFn leaf) {
   int bi;
-  const Key k = child_scan<G>(tree, geo, 1, q, w.lane, leaf, &bi);
+  const Key k = child_scan<G>(t, geo, 1, q, w.lane, leaf, &bi);
   int best;
   const Key m = w.max_key_minidx(k, bi, &best);
   if (w.lane == 0) {
-    tree[geo.off[1] + q] = m;
-    idx1[q] = best;
+    L1Node<Key> nd;
+    nd.k = m;
+    nd.i = best;
+    t.l1[q] = nd;
   }
 }
 
-// Recompute the ancestors (levels >= 2) of the level-1 groups dl[0..n).
+// Recompute the level-1 groups rec[0..n) from their leaves.  With G = 32 the
+// leaf loads of up to 4 groups are issued together (one memory round trip for
+// them, instead of one per group), then reduced group by group.
 template <int G, typename Key, typename LeafFn>
-__device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int* dl2, int n, const Grp<G>& w,
-                                   LeafFn leaf) {
+__device__ void group_recompute_list(const TreeRef<Key>& t, const TreeGeom& geo, const int* rec, int n,
+                                     const Grp<G>& w, LeafFn leaf) {
+  if (G != 32) {
+    for (int i = 0; i < n; ++i) group_recompute(t, geo, rec[i], w, leaf);
+    return;
+  }
+  for (int i0 = 0; i0 < n; i0 += 4) {
+    Key k[4];
+    int q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      q[j] = i0 + j < n ? rec[i0 + j] : -1;
+      k[j] = q[j] >= 0 ? child_key(t, geo, 0, q[j] * 32 + w.lane, leaf) : Key(0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (q[j] < 0) break;
+      int best;
+      const Key m = w.max_key_minidx(k[j], q[j] * 32 + w.lane, &best);
+      if (w.lane == 0) {
+        L1Node<Key> nd;
+        nd.k = m;
+        nd.i = best;
+        t.l1[q[j]] = nd;
+      }
+    }
+  }
+}
+
+// Recompute the ancestors (levels >= 2, shared memory) of the level-1 groups dl[0..n).
+template <int G, typename Key, typename LeafFn>
+__device__ void tree_fix_ancestors(const TreeRef<Key>& t, const TreeGeom& geo, int* dl, int* dl2, int n,
+                                   const Grp<G>& w, LeafFn leaf) {
   for (int l = 2; l <= geo.levels; ++l) {
     int cnt = 0;
     for (int base = 0; base < n; base += G) {
@@ -209,15 +274,15 @@ __device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int*
       cnt += __popc(bal);
     }
     w.sync();
-    int* t = dl;
+    int* tmp = dl;
     dl = dl2;
-    dl2 = t;
+    dl2 = tmp;
     n = cnt;
     for (int i = 0; i < n; ++i) {
       const int q = dl[i];
       int bi;
-      const Key m = w.max_key_only(child_scan<G>(tree, geo, l, q, w.lane, leaf, &bi));
-      if (w.lane == 0) tree[geo.off[l] + q] = m;
+      const Key m = w.max_key_only(child_scan<G>(t, geo, l, q, w.lane, leaf, &bi));
+      if (w.lane == 0) t.up[up_off(geo, l) + q] = m;
     }
     w.sync();
   }
@@ -225,11 +290,11 @@ __device__ void tree_fix_ancestors(Key* tree, const TreeGeom& geo, int* dl, int*
 
 // Full recompute of the level-1 groups dl[0..n) and their ancestors.
 template <int G, typename Key, typename LeafFn>
-__device__ void tree_update_list(Key* tree, int* idx1, const TreeGeom& geo, int* dl, int* dl2, int n,
+__device__ void tree_update_list(const TreeRef<Key>& t, const TreeGeom& geo, int* dl, int* dl2, int n,
                                  const Grp<G>& w, LeafFn leaf) {
-  for (int i = 0; i < n; ++i) group_recompute(tree, idx1, geo, dl[i], w, leaf);
+  group_recompute_list(t, geo, dl, n, w, leaf);
   w.sync();
-  tree_fix_ancestors(tree, geo, dl, dl2, n, w, leaf);
+  tree_fix_ancestors(t, geo, dl, dl2, n, w, leaf);
 }
 
 // Incremental rule for one leaf e of group q getting key kk, applied to the
@@ -252,7 +317,7 @@ __device__ __forceinline__ bool leaf_rule(Key& Q, int& I, int e, Key kk) {
 // -1, new key kk), lanes of the same group serialised by a match_any leader.
 // Appends groups to recompute to rec[] and changed groups to dirty[].
 template <int G, typename Key>
-__device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Key kk, const Grp<G>& w, int* se,
+__device__ __forceinline__ void apply_leaf_updates(L1Node<Key>* L1, int e, Key kk, const Grp<G>& w, int* se,
                                                    Key* sk, int* rec, int& nrec, int* dirty, int& ndirty) {
   const int q = e >= 0 ? (e >> 5) : -1;
   se[w.lane] = e;
@@ -262,8 +327,9 @@ __device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Ke
   const bool leader = e >= 0 && (__ffs(peers) - 1) == w.lane;
   bool r = false, changed = false;
   if (leader) {
-    Key Q = L1[q];
-    int I = idx1[q];
+    const L1Node<Key> nd = L1[q];
+    Key Q = nd.k;
+    int I = nd.i;
     const Key Q0 = Q;
     const int I0 = I;
     unsigned m = peers;
@@ -273,8 +339,10 @@ __device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Ke
       r = leaf_rule(Q, I, se[s2], sk[s2]);
     }
     if (!r && (Q != Q0 || I != I0)) {
-      L1[q] = Q;
-      idx1[q] = I;
+      L1Node<Key> o;
+      o.k = Q;
+      o.i = I;
+      L1[q] = o;
     }
     changed = r || Q != Q0;
   }
@@ -287,26 +355,46 @@ __device__ __forceinline__ void apply_leaf_updates(Key* L1, int* idx1, int e, Ke
 }
 
 template <int G, typename Key, typename LeafFn>
-__device__ int tree_argmax(const Key* tree, const int* idx1, const TreeGeom& geo, const Grp<G>& w,
-                           LeafFn leaf) {
+__device__ int tree_argmax(const TreeRef<Key>& t, const TreeGeom& geo, const Grp<G>& w, LeafFn leaf) {
   const int L = geo.levels, s = geo.size[L];
-  const Key* top = tree + geo.off[L];
   Key bk = 0;
-  int bq = 0x7fffffff;
+  int bq = 0x7fffffff, bi = 0;
   for (int i = w.lane; i < s; i += G) {  // top level (<= 64 nodes)
-    const Key k = top[i];
-    if (k > bk || bq == 0x7fffffff) { bk = k; bq = i; }
+    Key k;
+    int li = 0;
+    if (L == 1) {
+      const L1Node<Key> nd = t.l1[i];
+      k = nd.k;
+      li = nd.i;
+    } else {
+      k = t.up[up_off(geo, L) + i];
+    }
+    if (k > bk || bq == 0x7fffffff) { bk = k; bq = i; bi = li; }
   }
   int q;
   w.max_key_minidx(bk, bq, &q);
-  for (int l = L - 1; l >= 1; --l) {
-    int bi;
-    const Key k = child_scan<G>(tree, geo, l + 1, q, w.lane, leaf, &bi);
+  if (L == 1) return w.shfl(bi, q % G);  // the lane that scanned node q holds its argmax leaf
+  for (int l = L - 1; l >= 2; --l) {
+    int b;
+    const Key k = child_scan<G>(t, geo, l + 1, q, w.lane, leaf, &b);
     int best;
-    w.max_key_minidx(k, bi, &best);
+    w.max_key_minidx(k, b, &best);
     q = best;
   }
-  return idx1[q];
+  // level-1 children of q: key and argmax leaf in one record per lane
+  Key ck = 0;
+  int cq = 0x7fffffff, ci = 0;
+  for (int c = w.lane; c < 32; c += G) {
+    const int child = q * 32 + c;
+    if (child < geo.size[1]) {
+      const L1Node<Key> nd = t.l1[child];
+      if (nd.k > ck || cq == 0x7fffffff) { ck = nd.k; cq = child; ci = nd.i; }
+    }
+  }
+  int best;
+  w.max_key_minidx(ck, cq, &best);
+  // the winning child was scanned by lane (best - 32q) % G; take its argmax leaf
+  return w.shfl(ci, (best - q * 32) % G);
 }
 
 // ------------------------------------------------------------ argmax scans
@@ -422,6 +510,20 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   const DevGraph& g = p.g;
   const Grp<G>& w = c.w;
   const int lane = c.lane;
+  const bool PT = CI || (TR && p.pt_on);  // pre_total upkeep (E:171); TR: traced build
+  // Memory round trips are the cost of an update (the chain is serial), so the
+  // loads are issued level by level: the edge's records (erec, two-hop table
+  // offsets) -> its VN's slots, the committed state, the two-hop items ->
+  // the V2C inputs and ALL two-hop inputs / C2V values / pre values together.
+  const bool tab = g.hop_items != nullptr;
+  int n_items = 0, hsp = 0;
+  if (tab) {
+    c.items = g.hop_items + g.hop_ptr[e_star];
+    n_items = g.hop_n[e_star];
+    hsp = g.hop_sbptr[e_star];
+  } else {
+    c.items = c.items_buf;
+  }
   const int4 er = g.erec[e_star];  // (m*, n*, vn_ptr[n*], d_v(n*))
   const int m_star = er.x, n_star = er.y;
   const int2 vr = make_int2(er.z, er.w);
@@ -432,6 +534,41 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   const T nv = c.pre[e_star];
   const T tot = c.total[n_star] + (nv - old);  // E:147
   const T cf = act ? c.c2v[adj.x] : T(0);
+  if (tab) {
+    // stage the two-hop inputs now: they do not depend on this update's V2C
+    // values (items exclude the V2C edges), and keep each item's C2V (and,
+    // with pre_total upkeep, its old pre) for the refresh; two items per pass
+    for (int t = lane; t < n_items; t += 2 * G) {
+      const int t2 = t + G;
+      const int4 r = c.items[t];
+      int4 r2 = r;
+      if (t2 < n_items) r2 = c.items[t2];
+      const T x = c.in[r.x], cg = c.c2v[r.x];
+      const T x2 = c.in[r2.x], cg2 = c.c2v[r2.x];
+      T op = T(0), op2 = T(0);
+      int j1 = 0, j2 = 0;
+      if (PT) {
+        op = c.pre[r.x];
+        op2 = c.pre[r2.x];
+        j1 = g.edge_vn[r.x];
+        j2 = g.edge_vn[r2.x];
+      }
+      c.stage[r.w + (r.x - r.y)] = x;
+      c.cg[t] = cg;
+      if (PT) {
+        c.opre[t] = op;
+        c.cj[t] = j1;
+      }
+      if (t2 < n_items) {
+        c.stage[r2.w + (r2.x - r2.y)] = x2;
+        c.cg[t2] = cg2;
+        if (PT) {
+          c.opre[t2] = op2;
+          c.cj[t2] = j2;
+        }
+      }
+    }
+  }
   if (p.dump_buf && c.cur_f == 0 && c.prop == p.dump_step) {
     if (CI)
       for (int n = lane; n < g.N; n += G) {
@@ -453,21 +590,15 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     if (STORED) c.res[e_star] = T(0);
     c.total[n_star] = tot;
     if (CI) {
-      const T pt = p0(tot);  // cached p0(total) of n*, the only total that changes
+      const T pt = p0_cache(tot);  // cached p0(total) of n*, the only total that changes
       c.p0t[n_star] = pt;
-      const T cv = Num<T>::abs_(pt - p0(c.pretot[n_star]));  // E:148-149
+      const T cv = ci_cached(pt, c.pretot[n_star]);  // E:148-149
       c.ci[n_star] = cv;
       if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
     }
   }
   // V2C to the other checks of n* (E:153-160), also staged; slots in chunks of G
-  int n_items = 0, ci_ = 0, cs_ = 0;
-  if (g.hop_items) {
-    c.items = g.hop_items + g.hop_ptr[e_star];
-    n_items = g.hop_n[e_star];
-  } else {
-    c.items = c.items_buf;
-  }
+  int ci_ = 0, cs_ = 0;
   for (int k0 = 0; k0 < vr.y; k0 += G) {
     int4 a2 = adj;
     bool act2 = act;
@@ -480,25 +611,26 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       cf2 = act2 ? c.c2v[a2.x] : T(0);
     }
     int sbase = 0;
-    if (g.hop_items) {
-      if (k0 + lane < vr.y) sbase = g.hop_sb[g.hop_sbptr[e_star] + k0 + lane];
+    if (tab) {
+      if (k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
     } else {
       n_items = build_items_from<T, G>(c, a2, act2, &sbase, ci_, cs_);
     }
     if (act2) {
       const T v = clampv(tot - cf2);
-      const T th = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+      const T th = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;
       c.in[a2.x] = th;
       c.stage[sbase + (a2.x - a2.z)] = th;
     }
   }
   w.sync();
-  for (int t = lane; t < n_items; t += G) {  // stage the rest of each check
-    int4 r = c.items[t];
-    c.stage[r.w + (r.x - r.y)] = c.in[r.x];
+  if (!tab) {
+    for (int t = lane; t < n_items; t += G) {  // stage the rest of each check
+      int4 r = c.items[t];
+      c.stage[r.w + (r.x - r.y)] = c.in[r.x];
+    }
+    w.sync();
   }
-  w.sync();
-  const bool PT = CI || (TR && p.pt_on);  // pre_total upkeep (E:171); TR: traced build
   const bool dup = PT && g.hop_dup[e_star] != 0;
   // two-hop refresh (E:161-176), G edges per pass in reference order
   for (int base = 0; base < n_items; base += G) {
@@ -510,18 +642,18 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       const int4 r = c.items[t];
       const int ge = r.x, skip = r.x - r.y;
       // independent loads first (the pre[] store below would otherwise pin them)
-      const T cg = c.c2v[ge];
+      const T cg = tab ? c.cg[t] : c.c2v[ge];
       T opre = T(0);
       if (PT) {
-        j = g.edge_vn[ge];
-        opre = c.pre[ge];
+        j = tab ? c.cj[t] : g.edge_vn[ge];
+        opre = tab ? c.opre[t] : c.pre[ge];
       }
       const T* s = c.stage + r.w;
       T np_;
       if (KERNEL == KERNEL_EXACT) {
-        T prod = T(1);
+        T prod = cn_one<T>();
         for (int q = 0; q < r.z; ++q)
-          if (q != skip) prod *= s[q];
+          if (q != skip) prod = cn_mul(prod, s[q]);
         np_ = atanh_msg(prod, r.z - 1);
       } else {
         T sign = T(1), mag = Num<T>::kBig;
@@ -545,8 +677,12 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           T pt = c.pretot[j] + delta;  // E:171
           c.pretot[j] = pt;
           if (CI) {
-            const T cv = Num<T>::abs_(c.p0t[j] - p0(pt));  // E:173 (p0(total[j]) cached)
+            const T cv = ci_cached(c.p0t[j], pt);  // E:173 (p0(total[j]) cached)
             c.ci[j] = cv;
+            if (CT) {  // (VN, CI key) of this item for the CI-tree update
+              c.cj[t] = j;
+              c.ck[t] = Num<T>::key(cv);
+            }
             if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
           }
         }
@@ -561,105 +697,130 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         }
         const bool last = valid && ((peers >> lane) >> 1) == 0;
         if (CI && last) {
-          const T cv = Num<T>::abs_(c.p0t[j] - p0(c.pretot[j]));
+          const T cv = ci_cached(c.p0t[j], c.pretot[j]);
           c.ci[j] = cv;
+          if (CT) c.ck[t] = Num<T>::key(cv);
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
         }
+        if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
       }
     }
   }
   w.sync();
   if (RT) {
-    // incremental residual-tree update: e* first (residual -> 0), then one
-    // segment per 32-leaf group of the (ascending) items applies the leaf rule;
-    // groups whose argmax leaf decreased are recomputed from their leaves.
+    // incremental residual-tree update.  The leaf changes (e* -> 0, then the
+    // items' new residuals; items ascend, so each 32-leaf group's items form one
+    // run) are applied group by group, all groups in parallel: one lane per
+    // group loads the level-1 node (one memory round trip for all of them),
+    // folds in its changes and writes it back; groups whose argmax leaf
+    // decreased below the new maximum are recomputed from their leaves.
     const TreeGeom& geo = p.rgeo;
-    Key* L1 = c.rtree + geo.off[1];
-    int nrec = 0, ndirty = 0;
-    {
-      const int q = e_star >> 5;
-      Key Q = L1[q];
-      int I = c.ridx[q];
-      const Key Q0 = Q;
-      const bool rec = leaf_rule(Q, I, e_star, Num<T>::key(T(0)));
-      w.sync();
-      if (lane == 0) {
-        if (rec) c.dl1[nrec] = q;
-        else {
-          L1[q] = Q;
-          c.ridx[q] = I;
-        }
-        if (rec || Q != Q0) c.dl0[ndirty] = q;
-      }
-      nrec += rec ? 1 : 0;
-      ndirty += (rec || Q != Q0) ? 1 : 0;
-      w.sync();
-    }
+    L1Node<Key>* L1 = c.rt.l1;
+    int* segs = (int*)c.stage;  // stage is free again: run starts + sentinel
+    const int qs = e_star >> 5;
+    int nseg = 0;
+    bool covered = false;
     for (int base = 0; base < n_items; base += G) {
       const int t = base + lane;
       const bool valid = t < n_items;
-      const int e = valid ? c.items[t].x : -1;
-      const int q = valid ? (e >> 5) : -1;
-      const Key kk = valid ? c.nk[t] : Key(0);
-      // lanes of one group form a contiguous segment (items ascend); reduce it
-      const unsigned peers = w.match_any(q);
-      const bool leader = valid && (__ffs(peers) - 1) == lane;
-      Key Q = 0;
-      int I = 0;
-      if (valid) {
-        Q = L1[q];
-        I = c.ridx[q];
-      }
-      // the group's argmax leaf decreased -> recompute from leaves
-      const bool dec = valid && ((e == I && kk < Q) || p.dbg_full_tree);
-      const bool rec = (w.ballot(dec) & peers) != 0;
-      // segment max of the new keys, lowest edge among ties
-      int bi;
-      const Key km = warp_max_key_minidx_masked(kk, e, peers << w.base, &bi);
-      bool changed = false;
-      if (leader) {
-        if (rec) changed = true;
-        else if (km > Q || (km == Q && bi < I)) {
-          changed = km > Q;
-          L1[q] = km;
-          c.ridx[q] = bi;
+      const int q = valid ? (c.items[t].x >> 5) : -1;
+      const int qp = (valid && t > 0) ? (c.items[t - 1].x >> 5) : -2;
+      const bool start = valid && q != qp;
+      const unsigned bal = w.ballot(start);
+      if (start) segs[nseg + __popc(bal & w.lt)] = t;
+      nseg += __popc(bal);
+      covered = covered || w.any(start && q == qs);
+    }
+    if (lane == 0) segs[nseg] = n_items;
+    w.sync();
+    const int nrun = nseg + (covered ? 0 : 1);  // + e*'s group alone
+    const Key k0 = Num<T>::key(T(0));
+    int nrec = 0, ndirty = 0;
+    for (int s0 = 0; s0 < nrun; s0 += G) {
+      const int si = s0 + lane;
+      bool rec = false, changed = false;
+      int q = -1;
+      if (si < nrun) {
+        int a = 0, b = 0;
+        if (si < nseg) {
+          a = segs[si];
+          b = segs[si + 1];
+          q = c.items[a].x >> 5;
+        } else {
+          q = qs;
         }
+        const L1Node<Key> nd = L1[q];
+        const Key Q = nd.k;
+        const int I = nd.i;
+        // fold the run's changes: max new key mx (lowest leaf mi), and the
+        // new key of the argmax leaf I if it changed
+        Key mx = 0, nI = 0;
+        int mi = 0x7fffffff;
+        bool hasI = false;
+        if (q == qs) {
+          mx = k0;
+          mi = e_star;
+          if (e_star == I) { hasI = true; nI = k0; }
+        }
+        for (int t = a; t < b; ++t) {
+          const int e = c.items[t].x;
+          const Key kk = c.nk[t];
+          if (kk > mx || (kk == mx && e < mi)) { mx = kk; mi = e; }
+          if (e == I) { hasI = true; nI = kk; }
+        }
+        Key Qn = Q;
+        int In = I;
+        if (hasI && nI < Q && !(mx > Q)) {
+          rec = true;  // the maximum may now sit among unchanged leaves
+        } else if (mx > Q) {
+          Qn = mx;
+          In = mi;
+        } else if (mx == Q && mi < I) {
+          In = mi;
+        }
+        if (p.dbg_full_tree) rec = true;
+        if (!rec && (Qn != Q || In != I)) {
+          L1Node<Key> o;
+          o.k = Qn;
+          o.i = In;
+          L1[q] = o;
+        }
+        changed = rec || Qn != Q;
       }
-      const bool lrec = leader && rec;
-      const unsigned rb = w.ballot(lrec), cb = w.ballot(changed);
-      if (lrec) c.dl1[nrec + __popc(rb & w.lt)] = q;
+      const unsigned rb = w.ballot(rec), cb = w.ballot(changed);
+      if (rec) c.dl1[nrec + __popc(rb & w.lt)] = q;
       if (changed) c.dl0[ndirty + __popc(cb & w.lt)] = q;
       nrec += __popc(rb);
       ndirty += __popc(cb);
-      w.sync();
     }
-    auto rleaf = [&](int e) -> Key { return res_key<T, STORED, G>(c, e); };
-    for (int i = 0; i < nrec; ++i) group_recompute(c.rtree, c.ridx, geo, c.dl1[i], w, rleaf);
     w.sync();
-    if (geo.levels > 1) tree_fix_ancestors(c.rtree, geo, c.dl0, c.dl1, ndirty, w, rleaf);
+    auto rleaf = [&](int e) -> Key { return res_key<T, STORED, G>(c, e); };
+    group_recompute_list(c.rt, geo, c.dl1, nrec, w, rleaf);
+    w.sync();
+    if (geo.levels > 1) tree_fix_ancestors(c.rt, geo, c.dl0, c.dl1, ndirty, w, rleaf);
   }
   if (CT) {  // incremental CI-tree update: n* first, then the two-hop VNs
     const TreeGeom& geo = p.cgeo;
-    Key* L1 = c.ctree + geo.off[1];
+    L1Node<Key>* L1 = c.ct.l1;
     int* se = (int*)c.stage;  // stage is free again: G (index, key) pairs
     Key* sk = (Key*)(se + 32);
     int nrec = 0, ndirty = 0;
-    apply_leaf_updates(L1, c.cidx, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
+    apply_leaf_updates(L1, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
                        c.dl0, ndirty);
-    for (int base = 0; base < n_items; base += G) {
+    for (int base = 0; base < n_items; base += G) {  // (VN, key) pairs staged by the refresh
       const int t = base + lane;
       int j = -1;
       Key kk = 0;
       if (t < n_items) {
-        j = g.edge_vn[c.items[t].x];
-        kk = Num<T>::key(c.ci[j]);
+        j = c.cj[t];
+        kk = j >= 0 ? c.ck[t] : Key(0);
       }
-      apply_leaf_updates(L1, c.cidx, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
+      apply_leaf_updates(L1, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
     }
     auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
-    for (int i = 0; i < nrec; ++i) group_recompute(c.ctree, c.cidx, geo, c.dl1[i], w, cleaf);
+    group_recompute_list(c.ct, geo, c.dl1, nrec, w, cleaf);
     w.sync();
-    if (geo.levels > 1) tree_fix_ancestors(c.ctree, geo, c.dl0, c.dl1, ndirty, w, cleaf);
+    if (geo.levels > 1) tree_fix_ancestors(c.ct, geo, c.dl0, c.dl1, ndirty, w, cleaf);
   }
   if (MG && p.fast_sel) w.sync();
   c.cnt[C_PROP] += 1;
@@ -1097,7 +1258,7 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
   for (int e = lane; e < g.E; e += G) {
     T v = clampv(chl(g.edge_vn[e]));
     c.c2v[e] = T(0);
-    c.in[e] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+    c.in[e] = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;
   }
   for (int n = lane; n < g.N; n += G) c.total[n] = chl(n);
   c.w.sync();
@@ -1112,9 +1273,9 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
       c.pretot[n] = acc;  // E:121-125
       if (CI) {
-        const T pt = p0(c.total[n]);
+        const T pt = p0_cache(c.total[n]);
         c.p0t[n] = pt;
-        c.ci[n] = Num<T>::abs_(pt - p0(acc));
+        c.ci[n] = ci_cached(pt, acc);
       }
     }
   if ((kind == KIND_ME_CIRBP || kind == KIND_ME_LMD_CIRBP) && p.fast_sel) {
@@ -1144,8 +1305,8 @@ __device__ void me_topm_registers(const DynParams& p, Ctx<T, G>& c, int m, LeafF
   using Key = typename Num<T>::Key;
   constexpr int kBad = 0x7fffffff;
   const int lane = c.lane, s = p.rgeo.size[1], E = p.g.E;
-  const Key* L1 = c.rtree + p.rgeo.off[1];
-  Key k0 = lane < s ? L1[lane] : Key(0), k1 = lane + 32 < s ? L1[lane + 32] : Key(0);
+  const L1Node<Key>* L1 = c.rt.l1;
+  Key k0 = lane < s ? L1[lane].k : Key(0), k1 = lane + 32 < s ? L1[lane + 32].k : Key(0);
   bool v0 = lane < s, v1 = lane + 32 < s;
   int gq[4] = {kBad, kBad, kBad, kBad};
   int ng = 0;
@@ -1224,9 +1385,9 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
 
   switch (kind) {
     case KIND_RBP: {  // E:355-385
-      tree_build(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
+      tree_build(c.rt, p.rgeo, c.w, rleaf);
       while (c.prop < budget) {
-        int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
+        int e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
         c.cnt[C_CMP] += E - 1;
         propagate<T, KERNEL, false, true, false, false, G, false, TR>(p, c, e);
         ++c.prop;
@@ -1234,14 +1395,14 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       }
     } break;
     case KIND_CIRBP: {  // E:388-433
-      tree_build(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
+      tree_build(c.rt, p.rgeo, c.w, rleaf);
       const bool flat = p.flat_ci != 0;
-      if (!flat) tree_build(c.ctree, c.cidx, p.cgeo, c.w, cleaf);
+      if (!flat) tree_build(c.ct, p.cgeo, c.w, cleaf);
       const T gamma = (T)p.gamma;
       int kh = 0, kt = 0;  // per-iteration kappa tallies (warp-uniform)
       while (c.prop < budget) {
         const int it = c.it;
-        int n_star = flat ? argmax_scan<Key>(g.N, c.w, cleaf) : tree_argmax(c.ctree, c.cidx, p.cgeo, c.w, cleaf);
+        int n_star = flat ? argmax_scan<Key>(g.N, c.w, cleaf) : tree_argmax(c.ct, p.cgeo, c.w, cleaf);
         c.cnt[C_CMP] += g.N - 1 + 1;
         c.cnt[C_KTRIALS] += 1;
         ++kt;
@@ -1250,7 +1411,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         if (hit) {
           c.cnt[C_KHITS] += 1;
           ++kh;
-          e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, rleaf);
+          e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
           c.cnt[C_CMP] += E - 1;
         } else {
           e = argmax_vn_edges<T, G>(g, c, n_star);
@@ -1367,7 +1528,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       for (int e = lane; e < g.E; e += G) c.res[e] = Num<T>::abs_(c.pre[e] - c.c2v[e]);
       c.w.sync();
       auto sleaf = [&](int e) -> Key { return res_key<T, true, G>(c, e); };
-      tree_build(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
+      tree_build(c.rt, p.rgeo, c.w, sleaf);
       int boundary = 1;
       const int np_ = p.n_p < g.E ? p.n_p : g.E;
       // single-level residual tree (<= 64 groups of 32 leaves) and M <= 4: the
@@ -1387,7 +1548,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       }
       while (boundary <= I && !conv) {
         for (int t = 0; t < np_; ++t) {
-          int e = tree_argmax(c.rtree, c.ridx, p.rgeo, c.w, sleaf);
+          int e = tree_argmax(c.rt, p.rgeo, c.w, sleaf);
           if (lane == 0) {
             c.sel[t] = e;
             c.tmp[t] = c.res[e];
@@ -1395,14 +1556,14 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
             c.dl0[0] = e >> 5;
           }
           c.w.sync();
-          tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, 1, c.w, sleaf);
+          tree_update_list(c.rt, p.rgeo, c.dl0, c.dl1, 1, c.w, sleaf);
         }
         for (int t = lane; t < np_; t += G) {
           c.res[c.sel[t]] = c.tmp[t];
           c.dl0[t] = c.sel[t] >> 5;
         }
         c.w.sync();
-        tree_update_list(c.rtree, c.ridx, p.rgeo, c.dl0, c.dl1, np_, c.w, sleaf);
+        tree_update_list(c.rt, p.rgeo, c.dl0, c.dl1, np_, c.w, sleaf);
         c.cnt[C_CMP] += E - 1;
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
@@ -1441,15 +1602,16 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   const int fpb = (blockDim.x >> 5) * FPW;
   const int fr = (threadIdx.x >> 5) * FPW + (threadIdx.x & 31) / G;  // frame slot in the block
   const long long gf = (long long)blockIdx.x * fpb + fr;
-  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes;
-  // shared bytes per frame and HBM bytes per frame for this mode
-  const long long sh = (MODE == 0 ? sE + sN + sT : MODE == 1 ? sN + sT : MODE == 2 ? sT : 0);
+  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes, sU = p.slotU_bytes;
+  // shared bytes per frame (the U part always) and HBM bytes per frame for this mode
+  const long long sh = (MODE == 0 ? sE + sN + sT : MODE == 1 ? sN + sT : MODE == 2 ? sT : 0) + sU;
   const long long hb = (MODE == 0 ? 0 : MODE == 1 ? sE : MODE == 2 ? sE + sN : sE + sN + sT);
   unsigned char* shw = smem + fr * sh;
   unsigned char* hbw = p.ws + gf * hb;
   unsigned char* bE = MODE == 0 ? shw : hbw;
   unsigned char* bN = MODE == 0 ? shw + sE : MODE == 1 ? shw : hbw + sE;
   unsigned char* bT = MODE == 0 ? shw + sE + sN : MODE == 1 ? shw + sN : MODE == 2 ? shw : hbw + sE + sN;
+  unsigned char* bU = shw + (sh - sU);
   unsigned char* scr = smem + (long long)fpb * sh + (long long)fr * p.scratch_bytes;
   using Key = typename Num<T>::Key;
   Ctx<T, G> c;
@@ -1468,14 +1630,18 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   c.members = (int*)(bN + p.o_members);
   c.sel = (int*)(bN + p.o_sel);
   c.chosen = (int*)(bN + p.o_chosen);
-  c.rtree = (Key*)(bT + p.o_rtree);
-  c.ridx = (int*)(bT + p.o_ridx);
-  c.ctree = (Key*)(bT + p.o_ctree);
-  c.cidx = (int*)(bT + p.o_cidx);
+  c.rt.l1 = (L1Node<Key>*)(bT + p.o_rl1);
+  c.rt.up = (Key*)(bU + p.o_rup);
+  c.ct.l1 = (L1Node<Key>*)(bT + p.o_cl1);
+  c.ct.up = (Key*)(bU + p.o_cup);
   c.items_buf = (int4*)(scr + p.so_items);
   c.items = c.items_buf;
   c.stage = (T*)(scr + p.so_stage);
   c.nk = (Key*)(scr + p.so_nk);
+  c.cg = (T*)(scr + p.so_nk);
+  c.opre = (T*)(scr + p.so_opre);
+  c.cj = (int*)(scr + p.so_cj);
+  c.ck = (Key*)(scr + p.so_ck);
   c.dl0 = (int*)(scr + p.so_dl0);
   c.dl1 = (int*)(scr + p.so_dl1);
   c.sizes = (int*)(scr + p.so_sizes);

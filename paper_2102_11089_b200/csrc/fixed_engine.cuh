@@ -65,9 +65,9 @@ struct FixedParams {
 template <typename T, int KERNEL>
 __device__ __forceinline__ T tile_out(const T* in_s, int2 ck, int el, int lane) {
   if (KERNEL == KERNEL_EXACT) {
-    T prod = T(1);
+    T prod = cn_one<T>();
     for (int q = ck.x; q < ck.y; ++q)
-      if (q != el) prod *= in_s[q * kFixedFrames + lane];
+      if (q != el) prod = cn_mul(prod, in_s[q * kFixedFrames + lane]);
     return atanh_msg(prod, ck.y - ck.x - 1);
   } else {
     T sign = T(1), mag = Num<T>::kBig;
@@ -118,25 +118,25 @@ __device__ __forceinline__ void check_outputs_d(const int* te_vn, const T* in_s,
     constexpr bool kSuffix = sizeof(T) == 4;
     T suf[D];
     if (kSuffix) {
-      T acc = T(1);
+      T acc = cn_one<T>();
 #pragma unroll
       for (int q = D - 1; q >= 0; --q) {
         suf[q] = acc;
-        acc *= in[q];
+        acc = cn_mul(acc, in[q]);
       }
     }
-    T pre = T(1);
+    T pre = cn_one<T>();
 #pragma unroll
     for (int q = 0; q < D; ++q) {
       T prod = pre;
       if (kSuffix) {
-        prod *= suf[q];
+        prod = cn_mul(prod, suf[q]);
       } else {
 #pragma unroll
-        for (int r = q + 1; r < D; ++r) prod *= in[r];
+        for (int r = q + 1; r < D; ++r) prod = cn_mul(prod, in[r]);
       }
       const T out = atanh_msg(prod, D - 1);
-      pre *= in[q];
+      pre = cn_mul(pre, in[q]);
       if (act) commit_out<T, LAYERED>(te_vn, old_s, tot_s, la, ga, q, lane, out, c2v, total);
     }
   } else {
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(512, 2) fixed_decode_kernel(const __grid_const
             const T* st = so + kTileEdges * F;  // total rows
             for (int x = tid; x < ne * F; x += nt) {  // phase A from shared memory
               const T v = clampv(st[x] - so[x]);
-              in_s[x] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;  // E:58 / E:73
+              in_s[x] = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;  // E:58 / E:73
             }
             __syncthreads();
             if (sizeof(T) == 4) {  // one warp per check (shared prefix products)
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(512, 2) fixed_decode_kernel(const __grid_const
               const int el = el0 + u * nw;
               if (el < ne) {
                 const T v = clampv(tv[u] - o[u]);
-                in_s[el * F + lane] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;  // E:58 / E:73
+                in_s[el * F + lane] = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;  // E:58 / E:73
                 if (LAYERED) old_s[el * F + lane] = o[u];
               }
             }

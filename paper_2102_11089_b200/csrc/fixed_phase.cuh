@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_check_kernel(const __grid
     __syncthreads();
     for (int x = tid; x < ne * F; x += nt) {  // phase A: check inputs (E:58 / E:73)
       const T v = clampv(st[x] - so[x]);
-      in_s[x] = (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+      in_s[x] = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;
     }
     __syncthreads();
     const bool act = (am >> lane) & 1u;

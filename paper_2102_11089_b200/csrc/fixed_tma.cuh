@@ -124,7 +124,7 @@ struct SignSink {
 template <typename T, int KERNEL>
 __device__ __forceinline__ T staged_in(const T* so, const T* st, int x) {
   const T v = clampv(st[x] - so[x]);
-  return (KERNEL == KERNEL_EXACT) ? Num<T>::tanh_(T(0.5) * v) : v;
+  return (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;
 }
 
 // Output of staged row r (lane = frame): c2v row e0 + r; layered also commits
@@ -172,24 +172,24 @@ __device__ __forceinline__ void strip_check_d(const T* so, const T* st, const in
     constexpr bool kSuffix = sizeof(T) == 4;
     T suf[D];
     if (kSuffix) {
-      T acc = T(1);
+      T acc = cn_one<T>();
 #pragma unroll
       for (int q = D - 1; q >= 0; --q) {
         suf[q] = acc;
-        acc *= in[q];
+        acc = cn_mul(acc, in[q]);
       }
     }
-    T pre = T(1);
+    T pre = cn_one<T>();
 #pragma unroll
     for (int q = 0; q < D; ++q) {
       T prod = pre;
       if (kSuffix) {
-        prod *= suf[q];
+        prod = cn_mul(prod, suf[q]);
       } else {
 #pragma unroll
-        for (int r = q + 1; r < D; ++r) prod *= in[r];
+        for (int r = q + 1; r < D; ++r) prod = cn_mul(prod, in[r]);
       }
-      pre *= in[q];
+      pre = cn_mul(pre, in[q]);
       strip_commit_p<T, LAYERED>(so, st, tv, q * k + c, x0 + q * xs, c0 + q * xs, atanh_msg(prod, D - 1), total, lane,
                                  act, sk);
     }
@@ -231,9 +231,9 @@ __device__ __noinline__ void strip_check_generic(const T* so, const T* st, const
   for (int q = 0; q < d; ++q) {
     T out;
     if (KERNEL == KERNEL_EXACT) {
-      T prod = T(1);
+      T prod = cn_one<T>();
       for (int r = 0; r < d; ++r)
-        if (r != q) prod *= staged_in<T, KERNEL>(so, st, (r * k + c) * F + lane);
+        if (r != q) prod = cn_mul(prod, staged_in<T, KERNEL>(so, st, (r * k + c) * F + lane));
       out = atanh_msg(prod, d - 1);
     } else {
       T sign = T(1), mag = Num<T>::kBig;

@@ -15,7 +15,7 @@ namespace ldpc {
 
 template <typename T, int KERNEL>
 __device__ __forceinline__ T msg_in(T v) {  // cached check input (E:58 / E:73)
-  return KERNEL == KERNEL_EXACT ? Num<T>::tanh_(T(0.5) * v) : v;
+  return KERNEL == KERNEL_EXACT ? cn_in<T>(v) : v;
 }
 
 // in[e] = input of edge e from the extrinsic clamp(total - c2v) (E:754), all edges

@@ -238,11 +238,14 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.flat_ci = N <= kFlatCiMax ? 1 : 0;
   const bool rt = s->kind == KIND_RBP || s->kind == KIND_CIRBP || s->kind == KIND_ME_RBP;
   const bool ct = s->kind == KIND_CIRBP && !p.flat_ci;
-  p.o_rtree = take(rt ? p.rgeo.total * (long long)sizeof(Key) : 0);
-  p.o_ridx = take(rt ? p.rgeo.size[1] * 4ll : 0);
-  p.o_ctree = take(ct ? p.cgeo.total * (long long)sizeof(Key) : 0);
-  p.o_cidx = take(ct ? p.cgeo.size[1] * 4ll : 0);
+  p.o_rl1 = take(rt ? p.rgeo.size[1] * (long long)sizeof(L1Node<Key>) : 0);
+  p.o_cl1 = take(ct ? p.cgeo.size[1] * (long long)sizeof(L1Node<Key>) : 0);
   p.slotT_bytes = align16(o);
+  // U part (always shared memory): tree levels >= 2
+  o = 0;
+  p.o_rup = take(rt ? (p.rgeo.total - p.rgeo.size[1]) * (long long)sizeof(Key) : 0);
+  p.o_cup = take(ct ? (p.cgeo.total - p.cgeo.size[1]) * (long long)sizeof(Key) : 0);
+  p.slotU_bytes = align16(o);
   // per-warp shared scratch
   long long so = 0;
   auto stake = [&](long long bytes) {
@@ -251,9 +254,12 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
     return r;
   };
   const long long dl = std::max<long long>(G->max_items + 2, np + 1);
-  p.so_items = (int)stake((long long)G->max_items * 16);
+  p.so_items = (int)stake(G->d.hop_items ? 0 : (long long)G->max_items * 16);  // items built on the fly
   p.so_stage = (int)stake(std::max<long long>(((long long)G->max_items + 32) * sizeof(T), 32 * (4 + sizeof(Key))));
-  p.so_nk = (int)stake((long long)G->max_items * sizeof(Key));
+  p.so_nk = (int)stake((long long)G->max_items * std::max(sizeof(Key), sizeof(T)));  // keys; staged C2V values
+  p.so_opre = (int)stake(ci || s->want_trace ? (long long)G->max_items * sizeof(T) : 0);
+  p.so_cj = (int)stake(ci || s->want_trace ? (long long)G->max_items * 4 : 0);
+  p.so_ck = (int)stake(ct ? (long long)G->max_items * sizeof(Key) : 0);
   p.so_dl0 = (int)stake(dl * 4);
   p.so_dl1 = (int)stake(dl * 4);
   p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
@@ -285,7 +291,7 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
   DynParams& p = pl.p;
   dyn_layout<T>(G, s, p);
   const long long optin = smem_optin() - 1024;
-  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes, sc = p.scratch_bytes;
+  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes, sc = p.scratch_bytes + p.slotU_bytes;
   const long long sh[4] = {sE + sN + sT + sc, sN + sT + sc, sT + sc, sc};  // shared bytes per frame
   const long long hb[4] = {0, sE, sE + sN, sE + sN + sT};                 // HBM bytes per frame
   struct Cand { int mode, g16, wpb; long long smem; int occ; long long frames; };
