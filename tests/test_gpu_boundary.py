@@ -53,18 +53,6 @@ def test_two_streams_concurrently(kind):
             np.testing.assert_array_equal(gb[key], ref_b[key], err_msg=key)
 
 
-@pytest.mark.parametrize("kind", ["rbp", "cirbp", "me_cirbp"])
-def test_lane_variants_match(kind):
-    """Dynamic engine: 32 lanes per frame == 16 lanes per frame (2 frames per warp)."""
-    spec, g = load_code("C1")
-    llrs = torch.from_numpy(llr_batch(spec, 2.0, seed=4, start=0, count=700)).cuda()
-    cfg = ScheduleConfig(kind=kind, i_max=3, n_p=4)
-    a = results_to_numpy(decode_batch(spec, llrs, cfg, variant="lanes32"), kind, 3)
-    b = results_to_numpy(decode_batch(spec, llrs, cfg, variant="lanes16"), kind, 3)
-    for key in ("u_hat", "prop", "counters", "bit_errors_at"):
-        np.testing.assert_array_equal(a[key], b[key], err_msg=key)
-
-
 def test_variant_bits_validated():
     from paper_2102_11089_b200 import _native
     spec, g = load_code("C0")
