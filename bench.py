@@ -3,15 +3,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload C0|C1|C2|C3|C4|C3F]
 
-Workload (default): BASELINE.json configs[3] -- the largest single-GPU config,
-the BG1-shaped n=26112 QC code (Z=384, 2Z punctured), BPSK-AWGN at Eb/N0 =
-1.0 dB, budget i_max = 10 (10 E C2V updates), batch 10,000 frames, float64
-(the reference's arithmetic), schedules flooding, layered, RBP, CIRBP and
-ME-CIRBP M=64.  One step = the batch decoded once by every schedule.  value =
-total C2V edge updates / time over the K timed steps (whole job, all ranks).
-The batch's LLRs (1.04 GB) exceed the 126 MB L2, so every step streams its
-inputs from HBM.  The C1 workload (configs[1], every schedule, 100k frames)
-is measured in the same run as a secondary block (`secondary`, 2 steps).
+Workload (default): BASELINE.json configs[1] -- the WiFi-shaped n=648 QC code
+(Z=27), BPSK-AWGN at Eb/N0 = 2.0 dB (mid-sweep), i_max = 3, batch 100,000
+frames, float64 (the reference's arithmetic), and every schedule the config
+names (flooding, layered, RBP, CIRBP, LMDRBP, sLMDRBP, LMD-CIRBP, ME-CIRBP
+M=4, ME-RBP M=4).  One step = the batch decoded once by every schedule.
+value = total C2V edge updates / time over the K timed steps (whole job, all
+ranks).  The batch's LLRs (259 MB) exceed the 126 MB L2, so every step
+streams its inputs from HBM.
+
+The same run also measures BASELINE configs[3] -- the largest single-GPU
+config, the BG1-shaped n=26112 code (Z=384, 2Z punctured) at 1.0 dB, i_max 10,
+10,000 frames, flooding / layered / RBP / CIRBP / ME-CIRBP M=64 -- as the
+`secondary.C3` block with its own roofline, CPU legs and GPU==oracle identity
+(1 warm-up + 1 timed step: one C3 step is minutes of GPU time, so the driver's
+20 + 5 steps of it would not fit its time limit; `--workload C3` runs it as
+the main line).
 
 --impl reference: the reference's OWN decoder (ldpc_ids.schedules.decode,
 numba, installed unmodified in baseline/_ref) on all host cores through the
@@ -154,7 +161,9 @@ def run_reference(args, wl):
     spec = getattr(configs, f"make_{key.lower()}_code")()
     g = build_tanner(spec.h)
     cores = os.cpu_count() or 1
-    sample = args.ref_sample or cores
+    # one frame per core per step for the BG1-shaped code (seconds of CPU per
+    # frame), 2048 frames otherwise (the same order of CPU time per step)
+    sample = args.ref_sample or (cores if key == "C3" else min(batch, 2048))
     llr = make_inputs(spec, ebn0, 0, sample).astype(np.float64)
     use_ref = refpool.available() and not args.ref_port
     pool = refpool.RefPool(spec, scheds, i_max, workers=cores) if use_ref else None
@@ -285,17 +294,14 @@ def clopper_pearson(k, n, alpha=0.05):
 
 def run_ours(args, wl):
     rank, world, local = dist_setup(args)
+    cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
     line = measure(args, wl, args.workload, args.steps, args.warmup, rank, world, local,
-                   batch=args.batch, cpu=rank == 0 and world == 1 and not args.no_cpu_baseline)
-    if args.workload == "C3" and not args.no_secondary and not args.only:
-        # BASELINE configs[1] (C1, every schedule) on the same clock, 2 timed steps
-        sec = measure(args, WORKLOADS["C1"], "C1", 2, 3, rank, world, local, batch=0, cpu=False)
-        line["secondary"] = {"C1": {k: sec[k] for k in ("metric", "value", "unit", "steps", "warmup",
-                                                         "ms_per_step", "dtype", "config", "e2e",
-                                                         "gpu_launches", "roofline")},
-                             "C1_per_schedule": {k: {q: v[q] for q in ("ms", "edge_updates_per_s", "frames_per_s",
-                                                                        "fer")}
-                                                 for k, v in sec["per_schedule"].items()}}
+                   batch=args.batch, cpu=cpu)
+    if args.workload == "C1" and not args.no_secondary and not args.only:
+        # BASELINE configs[3] (C3, the BG1-shaped code at 10k frames) on the same
+        # clock: one step is minutes of GPU time, so 1 warm-up + 1 timed step
+        sec = measure(args, WORKLOADS["C3"], "C3", 1, 1, rank, world, local, batch=0, cpu=cpu, e2e=False)
+        line["secondary"] = {"C3": {k: sec[k] for k in sec if k not in ("e2e",)}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -303,7 +309,7 @@ def run_ours(args, wl):
         dist.destroy_process_group()
 
 
-def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=False):
+def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=False, e2e=True):
     import torch
     from paper_2102_11089_b200 import configs
     from paper_2102_11089_b200 import dist as D
@@ -378,7 +384,7 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
     torch.cuda.synchronize()
     e_start.record(stream)
     h2d = d2h = 0
-    for s in range(steps):
+    for s in range(steps if e2e else 0):
         src = llr_pinned.to(dev, non_blocking=True)
         h2d += llr_pinned.numel() * llr_pinned.element_size()
         for i, c in enumerate(cfgs):
@@ -394,7 +400,7 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
     t_max, e_max = (float(x) for x in D.all_max([total_ms, e2e_ms]))
     job_updates = step_updates * steps
     value = job_updates / (t_max / 1e3)
-    e2e_value = job_updates / (e_max / 1e3)
+    e2e_value = job_updates / (e_max / 1e3) if e2e else None
 
     # dominant kernel roofline (algorithmic state bytes / kernel time)
     dom = int(np.argmax(sched_ms))
@@ -437,7 +443,7 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
                              "time; the dynamic schedules are a serial update chain per frame "
                              "(latency-bound), so this fraction is low by construction" % args.precision},
         "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // steps,
-                "d2h_bytes_per_step": d2h // steps},
+                "d2h_bytes_per_step": d2h // steps} if e2e else None,
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -476,14 +482,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="C1", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--ref-port", action="store_true", help="reference arm on the C port even if baseline/_ref exists")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the C1 block of the default C3 run")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C3 block of the default C1 run")
     ap.add_argument("--only", default="", help="run one schedule of the workload (e.g. cirbp, me_rbp/M4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT"):

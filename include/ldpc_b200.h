@@ -168,6 +168,22 @@ int ldpc_last_launch_count(void);
 const char* ldpc_strerror(int code);
 int ldpc_version(void);
 
+/* Debug / audit: the GPU side of the reference's stepwise decoder state
+ * (kernels.py:98-181, DecoderState.propagate / recompute_all; the survey's
+ * ldpc_decode_replay).  Frame f is initialised like every schedule
+ * (_init_state, E:106-127) and then propagates the GIVEN edge sequence
+ * forced_edges[f][0..steps) (device int32) with pre_total and CI maintained
+ * (DecoderState(maintain_ci=True)), instead of selecting edges.  Device outputs:
+ *   c2v_trace[B][steps] float64: the C2V value each update commits (E:143);
+ *   state_out[B][2E+3N] float64: c2v, pre_c2v, total, pre_total, ci after the
+ *     last update (what recompute_all audits);
+ *   counters[B][8] int64 (order of _engine.py:17-25).
+ * s supplies kernel / precision / llr_f64 (kind and budget are ignored). */
+int ldpc_replay_workspace_size(const ldpc_graph_t* g, const ldpc_sched_t* s, int64_t B, size_t* bytes);
+int ldpc_decode_replay(const ldpc_graph_t* g, const void* llr, int64_t B, const ldpc_sched_t* s,
+                       const int32_t* forced_edges, int32_t steps, double* c2v_trace, double* state_out,
+                       int64_t* counters, void* workspace, size_t ws_bytes, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

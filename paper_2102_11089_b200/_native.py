@@ -43,7 +43,7 @@ def variant_bits(names):
 # every exported symbol of include/ldpc_b200.h
 EXPORTS = ("ldpc_graph_create", "ldpc_graph_destroy", "ldpc_graph_info", "ldpc_workspace_size",
            "ldpc_decode", "ldpc_decode_traced", "ldpc_select_vns", "ldpc_set_step_log", "ldpc_set_state_dump",
-           "ldpc_generate_awgn",
+           "ldpc_generate_awgn", "ldpc_replay_workspace_size", "ldpc_decode_replay",
            "ldpc_last_launch_count",
            "ldpc_strerror", "ldpc_version")
 
@@ -74,6 +74,8 @@ def lib():
     L.ldpc_set_step_log.argtypes = [P, I32]
     L.ldpc_generate_awgn.argtypes = [I32, I32, I64, C.c_double, C.c_uint64, I64, P, I32, P]
     L.ldpc_set_state_dump.argtypes = [I64, P]
+    L.ldpc_replay_workspace_size.argtypes = [P, C.POINTER(LdpcSched), I64, C.POINTER(SZ)]
+    L.ldpc_decode_replay.argtypes = [P, P, I64, C.POINTER(LdpcSched), P, I32, P, P, P, P, SZ, P]
     L.ldpc_last_launch_count.argtypes = []
     L.ldpc_strerror.argtypes = [C.c_int]
     L.ldpc_strerror.restype = C.c_char_p

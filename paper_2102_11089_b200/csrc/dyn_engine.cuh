@@ -1657,4 +1657,95 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   }
 }
 
+// ---------------------------------------------------------------- replay
+// Debug / audit path, the GPU side of the reference's stepwise DecoderState
+// (kernels.py:98-181): after _init_state (E:106-127) frame f propagates the
+// GIVEN edges forced[f][0..steps) (E:130-176, pre_total and CI maintained like
+// DecoderState(maintain_ci=True)), recording each update's committed C2V value
+// in trace[f][k]; then writes counters[f][8] and the state
+// out[f] = c2v[E], pre[E], total[N], pre_total[N], ci[N] (float64).  One warp
+// per frame (block), every state part in the HBM slot of the frame.  Replaying
+// the reference's own edge sequence ties GPU message values to the reference
+// update by update, independent of argmax near-ties.
+template <typename T, int KERNEL>
+__global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ DynParams p, const int* forced,
+                                                         int steps, double* trace, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using Key = typename Num<T>::Key;
+  const long long f = blockIdx.x;
+  if (f >= p.B) return;
+  const long long sE = p.slotE_bytes, sN = p.slotN_bytes, sT = p.slotT_bytes;
+  unsigned char* bE = p.ws + f * (sE + sN + sT);
+  unsigned char* bN = bE + sE;
+  unsigned char* bT = bN + sN;
+  unsigned char* bU = smem;
+  unsigned char* scr = smem + p.slotU_bytes;
+  Ctx<T, 32> c;
+  c.w = Grp<32>::make();
+  c.lane = c.w.lane;
+  c.c2v = (T*)(bE + p.o_c2v);
+  c.pre = (T*)(bE + p.o_pre);
+  c.in = (T*)(bE + p.o_in);
+  c.res = (T*)(bE + p.o_res);
+  c.total = (T*)(bN + p.o_total);
+  c.pretot = (T*)(bN + p.o_pretot);
+  c.ci = (T*)(bN + p.o_ci);
+  c.p0t = (T*)(bN + p.o_p0t);
+  c.tmp = (T*)(bN + p.o_tmp);
+  c.inpp = (uint8_t*)(bN + p.o_inpp);
+  c.members = (int*)(bN + p.o_members);
+  c.sel = (int*)(bN + p.o_sel);
+  c.chosen = (int*)(bN + p.o_chosen);
+  c.gid = (uint8_t*)(bN + p.o_gid);
+  c.gbits = (unsigned*)(bN + p.o_gbits);
+  c.rt.l1 = (L1Node<Key>*)(bT + p.o_rl1);
+  c.rt.up = (Key*)(bU + p.o_rup);
+  c.ct.l1 = (L1Node<Key>*)(bT + p.o_cl1);
+  c.ct.up = (Key*)(bU + p.o_cup);
+  c.items_buf = (int4*)(scr + p.so_items);
+  c.items = c.items_buf;
+  c.stage = (T*)(scr + p.so_stage);
+  c.nk = (Key*)(scr + p.so_nk);
+  c.cg = (T*)(scr + p.so_nk);
+  c.opre = (T*)(scr + p.so_opre);
+  c.cj = (int*)(scr + p.so_cj);
+  c.ck = (Key*)(scr + p.so_ck);
+  c.dl0 = (int*)(scr + p.so_dl0);
+  c.dl1 = (int*)(scr + p.so_dl1);
+  c.sizes = (int*)(scr + p.so_sizes);
+  c.hist = (int*)(scr + p.so_hist);
+  for (int k = 0; k < kCounters; ++k) c.cnt[k] = 0;
+  c.prop = 0;
+  c.cur_f = f;
+  c.nsel = 0;
+  c.rng = p.seed;
+  init_state<T, KERNEL, true, 32, false>(p, c, f, KIND_LMD_CIRBP);
+  for (int k = 0; k < steps; ++k) {
+    const int e = forced[f * steps + k];
+    if (c.lane == 0) trace[f * steps + k] = (double)c.pre[e];  // the value propagate commits (E:143)
+    c.w.sync();
+    propagate<T, KERNEL, true, false, false, false, 32, false, false>(p, c, e);
+    ++c.prop;
+  }
+  c.w.sync();
+  const DevGraph& g = p.g;
+  double* o = out + f * (2ll * g.E + 3ll * g.N);
+  for (int e = c.lane; e < g.E; e += 32) {
+    o[e] = (double)c.c2v[e];
+    o[g.E + e] = (double)c.pre[e];
+  }
+  for (int n = c.lane; n < g.N; n += 32) {
+    o[2 * g.E + n] = (double)c.total[n];
+    o[2 * g.E + g.N + n] = (double)c.pretot[n];
+    o[2 * g.E + 2 * g.N + n] = (double)c.ci[n];
+  }
+  if (c.lane < kCounters) {
+    long long v = 0;
+#pragma unroll
+    for (int k = 0; k < kCounters; ++k)
+      if (k == c.lane) v = c.cnt[k];
+    p.counters[f * kCounters + c.lane] = v;
+  }
+}
+
 }  // namespace ldpc

@@ -61,6 +61,7 @@ struct FixedTraceParams {
 };
 }  // namespace ldpc
 void* ldpc_fixed_trace_kernel(int f64, int kernel, int layered);
+void* ldpc_replay_kernel(int f64, int kernel);  // dyn_replay.cu
 
 // batch-wide phase kernels for flooding / layered (fixed_phase.cu)
 struct PhaseKernels {

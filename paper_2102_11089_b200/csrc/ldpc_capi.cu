@@ -766,6 +766,24 @@ __global__ void select_vns_kernel(const double* ci, const uint8_t* mask, int N, 
 
 // ================================================================== C ABI
 
+// replay helpers (ldpc_decode_replay below)
+namespace {
+template <typename T>
+void replay_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
+  ldpc_sched_t r = *s;
+  r.kind = KIND_LMD_CIRBP;  // a CI kind without trees: pre_total and CI maintained
+  r.want_trace = 0;
+  dyn_layout<T>(G, &r, p);
+}
+int replay_check(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
+  if (!G || !s || B < 0) return LDPC_ERR_INVALID;
+  if (s->kernel != KERNEL_EXACT && s->kernel != KERNEL_MINSUM) return LDPC_ERR_INVALID;
+  if (s->precision != LDPC_F64 && s->precision != LDPC_F32) return LDPC_ERR_INVALID;
+  if (G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
+  return LDPC_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int ldpc_version(void) { return 10000; }
@@ -1258,6 +1276,58 @@ int ldpc_select_vns(const double* ci, const uint8_t* mask, int32_t N, int32_t n_
   select_vns_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(ci, mask, N, n_g, n_p, seed, out, count_dev);
   g_last_launches = 1;
   return cuda_check(cudaGetLastError());
+}
+
+// ---- replay (debug / audit): DecoderState-style forced edge sequences
+
+
+int ldpc_replay_workspace_size(const ldpc_graph_t* G, const ldpc_sched_t* s, int64_t B, size_t* bytes) {
+  if (int rc = replay_check(G, s, B)) return rc;
+  if (!bytes) return LDPC_ERR_INVALID;
+  DynParams p;
+  memset(&p, 0, sizeof(p));
+  if (s->precision == LDPC_F64) replay_layout<double>(G, s, p);
+  else replay_layout<float>(G, s, p);
+  *bytes = (size_t)(256 + B * (p.slotE_bytes + p.slotN_bytes + p.slotT_bytes));
+  return LDPC_OK;
+}
+
+int ldpc_decode_replay(const ldpc_graph_t* G, const void* llr, int64_t B, const ldpc_sched_t* s,
+                       const int32_t* forced_edges, int32_t steps, double* c2v_trace, double* state_out,
+                       int64_t* counters, void* workspace, size_t ws_bytes, void* cuda_stream) {
+  g_last_launches = 0;
+  if (int rc = replay_check(G, s, B)) return rc;
+  if (steps < 0 || (B > 0 && (!llr || !state_out || !counters || (steps > 0 && (!forced_edges || !c2v_trace)))))
+    return LDPC_ERR_INVALID;
+  if (B == 0) return LDPC_OK;
+  size_t need = 0;
+  ldpc_replay_workspace_size(G, s, B, &need);
+  if (!workspace || ws_bytes < need) return LDPC_ERR_WORKSPACE;
+  DynParams p;
+  memset(&p, 0, sizeof(p));
+  const bool f64 = s->precision == LDPC_F64;
+  if (f64) replay_layout<double>(G, s, p);
+  else replay_layout<float>(G, s, p);
+  p.g = G->d;
+  p.kind = KIND_LMD_CIRBP;
+  p.kernel = s->kernel;
+  p.i_max = s->i_max;
+  p.k_info = s->k_info;
+  p.seed = s->selection_seed;
+  p.llr = llr;
+  p.llr_f64 = s->llr_f64;
+  p.B = B;
+  p.counters = (long long*)counters;
+  p.ws = (unsigned char*)workspace + 256;
+  const int smem = (int)(p.slotU_bytes + p.scratch_bytes);
+  if (smem > smem_optin() - 1024) return LDPC_ERR_UNSUPPORTED;
+  void* fn = ldpc_replay_kernel(f64 ? 1 : 0, s->kernel);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  void* args[] = {&p, (void*)&forced_edges, &steps, &c2v_trace, &state_out};
+  if (int rc = cuda_check(cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32), args, smem, (cudaStream_t)cuda_stream)))
+    return rc;
+  g_last_launches = 1;
+  return LDPC_OK;
 }
 
 }  // extern "C"

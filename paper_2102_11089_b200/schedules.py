@@ -340,6 +340,52 @@ decode_layered = _wrap(("layered",))
 decode_me_rbp = _wrap(("me_rbp",))
 
 
+def decode_replay(code, llrs, forced_edges, kernel="exact", precision="f64", k_info=None, stream=None):
+    """The GPU side of the reference's stepwise DecoderState (kernels.py:98-181):
+    each frame is initialised like every schedule (_init_state) and then
+    propagates the GIVEN edges forced_edges[B, steps] (pre_total and CI
+    maintained, like DecoderState(maintain_ci=True)) through ldpc_decode_replay.
+    Returns device tensors: c2v_trace [B, steps] float64 (the value each update
+    commits), c2v / pre_c2v [B, E], total / pre_total / ci [B, N] float64 (the
+    state recompute_all audits) and counters [B, 8] int64."""
+    if isinstance(code, CodeSpec):
+        k_info = code.k_info if k_info is None else k_info
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dg = device_graph(code, dev)
+    if not torch.is_tensor(llrs):
+        llrs = torch.from_numpy(np.ascontiguousarray(llrs))
+    llrs = llrs.to(dev).contiguous()
+    if llrs.dtype not in (torch.float32, torch.float64):
+        llrs = llrs.to(torch.float64)
+    if llrs.dim() != 2 or llrs.shape[1] != dg.N:
+        raise ValueError("channel LLR length mismatch")
+    fe = torch.as_tensor(np.ascontiguousarray(forced_edges), dtype=torch.int32).to(dev).contiguous()
+    B, steps = llrs.shape[0], int(fe.shape[1]) if fe.dim() == 2 else 0
+    if fe.dim() != 2 or fe.shape[0] != B:
+        raise ValueError("forced_edges must be [B, steps]")
+    if steps and (int(fe.min()) < 0 or int(fe.max()) >= dg.E):
+        raise ValueError("forced edge out of range")
+    cfg = ScheduleConfig(kind="rbp", kernel=kernel, precision=precision)
+    sched = _sched(cfg, int(k_info or 0), llrs.dtype == torch.float64)
+    L = _native.lib()
+    sz = C.c_size_t()
+    _native.check(L.ldpc_replay_workspace_size(dg.handle, C.byref(sched), B, C.byref(sz)),
+                  "ldpc_replay_workspace_size")
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(st):
+        ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=dev)
+        trace = torch.empty((B, max(steps, 1)), dtype=torch.float64, device=dev)
+        state = torch.empty((B, 2 * dg.E + 3 * dg.N), dtype=torch.float64, device=dev)
+        counters = torch.empty((B, 8), dtype=torch.int64, device=dev)
+    _native.check(L.ldpc_decode_replay(dg.handle, _ptr(llrs), B, C.byref(sched), _ptr(fe), steps, _ptr(trace),
+                                       _ptr(state), _ptr(counters), _ptr(ws), ws.numel(),
+                                       C.c_void_p(st.cuda_stream)), "ldpc_decode_replay")
+    E, N = dg.E, dg.N
+    return {"c2v_trace": trace[:, :steps], "c2v": state[:, :E], "pre_c2v": state[:, E:2 * E],
+            "total": state[:, 2 * E:2 * E + N], "pre_total": state[:, 2 * E + N:2 * E + 2 * N],
+            "ci": state[:, 2 * E + 2 * N:], "counters": counters, "_ws": ws}
+
+
 def decode_batch_logged(code, llrs, config: ScheduleConfig, log_cap=1000, **kw):
     """decode_batch plus the propagated edge of each of the first `log_cap`
     updates per frame ([B, log_cap] int64, -1 past the end) and the committed

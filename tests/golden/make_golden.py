@@ -190,7 +190,61 @@ def make_sim_golden():
                         bit_errors_at=np.array([str(r.bit_errors_at) for r in recs]))
 
 
+def _steps_work(task):
+    """One frame through the reference's stepwise DecoderState (kernels.py:98-181):
+    residual-argmax edge choice (lowest index among ties, like _decode_rbp),
+    propagate(edge) for `steps` updates; returns the edge sequence, the committed
+    C2V value of each update, the state after the last update and the
+    recompute_all audit of that state."""
+    code_key, llr, steps, kernel = task
+    rc, rs = _ref()
+    from ldpc_ids import kernels as rk
+    spec = {"C0": configs.make_c0_code, "C1": configs.make_c1_code, "C2": configs.make_c2_code}[code_key]()
+    rspec = _ref_spec(spec)
+    graph = rc.build_tanner(rspec.h)
+    st = rk.DecoderState(graph, np.asarray(llr, np.float64), kernel=kernel, maintain_ci=True)
+    edges, vals = [], []
+    for _ in range(steps):
+        e = int(np.argmax(st.residual))  # first maximum = lowest edge id
+        st.propagate(e)
+        edges.append(e)
+        vals.append(float(st.c2v[e]))
+    res, total, pre_total, ci = st.recompute_all()
+    c = st.counters
+    return dict(edges=np.array(edges, np.int32), c2v=np.array(vals),
+                s_c2v=st.c2v.copy(), s_pre=st.pre_c2v.copy(), s_total=st.total_llr.copy(),
+                s_pretot=st.pre_total_llr.copy(), s_ci=st.ci.copy(),
+                a_res=res, a_total=total, a_pretot=pre_total, a_ci=ci,
+                counters=np.array([c.c2v_propagations, c.v2c_updates, c.c2v_pre_updates, c.ci_updates,
+                                   c.residual_ci_comparisons, c.multi_select_comparisons, c.kappa_hits,
+                                   c.kappa_trials], np.int64))
+
+
+def make_steps_golden():
+    """steps.npz: per-update traces of the reference's DecoderState.propagate
+    (kernels.py:145-156) for the first 1000 updates of C0-C2 frames (exact and
+    min-sum), with the final state and its recompute_all audit (kernels.py:161-181)."""
+    _ref()
+    cases = [("C0", 2.0, 4, "exact"), ("C1", 2.0, 3, "exact"), ("C2", 1.0, 2, "exact"), ("C0", 2.0, 2, "minsum"),
+             ("C0", 6.0, 2, "exact"), ("C2", 5.0, 1, "exact")]
+    payload = {}
+    with ProcessPoolExecutor(max_workers=os.cpu_count()) as pool:
+        for ci_, (key, eb, nfr, kernel) in enumerate(cases):
+            spec = {"C0": configs.make_c0_code, "C1": configs.make_c1_code, "C2": configs.make_c2_code}[key]()
+            llrs = llr_batch(spec, eb, seed=0, start=500, count=nfr, dtype=np.float32)
+            res = list(pool.map(_steps_work, [(key, l, 1000, kernel) for l in llrs]))
+            payload[f"c{ci_}_case"] = np.array(repr(dict(code=key, ebn0=eb, kernel=kernel)))
+            payload[f"c{ci_}_llrs"] = llrs
+            for k in res[0]:
+                payload[f"c{ci_}_{k}"] = np.stack([r[k] for r in res])
+    payload["n_cases"] = np.int64(len(cases))
+    np.savez_compressed(OUT / "steps.npz", **payload)
+
+
 def main():
+    if "--only-steps" in sys.argv:
+        make_steps_golden()
+        return
     if "--only-trace" in sys.argv:
         make_trace_golden()
         return

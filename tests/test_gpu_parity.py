@@ -311,5 +311,5 @@ def test_fp32_messages_within_1e4_first_1000_updates(code_key, eb, n, kind):
         compared += k
         sat += int((np.abs(x) > 28.0).sum())
     assert compared >= 0.5 * n * 1000, compared
-    if eb >= 4.5:
-        assert sat > 0  # the saturated regime was exercised
+    if code_key == "C0" and eb >= 6.0:
+        assert sat > 0  # the saturated regime was exercised (|c2v| -> 28.3242)

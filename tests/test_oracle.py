@@ -136,3 +136,17 @@ def test_oracle_j_gamma_counts_match_reference():
                                   cfg["gamma"], cfg["n_p"], cfg["n_g"], cfg["selection_seed"],
                                   want_trace=True)["trace_llrs"] for row in llrs]
         np.testing.assert_array_equal(j_counts_from_traces(traces, gam), z["j_counts"][ci], err_msg=str(case))
+
+
+def test_oracle_rbp_equals_reference_stepwise_decoder():
+    """The reference's stepwise DecoderState (kernels.py:98-181) driven by the
+    first residual maximum is RBP (E:355-385): the oracle's RBP step log (edge,
+    committed C2V) reproduces tests/golden/steps.npz update for update."""
+    z = np.load("tests/golden/steps.npz")
+    for i in range(int(z["n_cases"])):
+        case = ast.literal_eval(str(z[f"c{i}_case"]))
+        spec, g = load_code(case["code"])
+        for f, llr in enumerate(z[f"c{i}_llrs"]):
+            r = pyoracle.decode(g, llr.astype(np.float64), "rbp", case["kernel"], 1, spec.k_info, log_cap=1000)
+            np.testing.assert_array_equal(r["log_edge"][:1000], z[f"c{i}_edges"][f], err_msg=str((case, f)))
+            np.testing.assert_array_equal(r["log_c2v"][:1000], z[f"c{i}_c2v"][f], err_msg=str((case, f)))
