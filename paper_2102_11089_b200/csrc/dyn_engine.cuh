@@ -97,6 +97,7 @@ struct DynParams {
   int flat_ci;            // CIRBP: flat CI argmax instead of a tree
   int scratch_bytes;      // per-warp shared scratch
   int so_items, so_stage, so_nk, so_opre, so_cj, so_ck, so_dl0, so_dl1, so_sizes, so_hist;
+  int dl_cap;             // entries of dl0 (twice that allocated: ping-pong for the levels >= 3 fix)
   int fast_sel;           // ME kinds with n_g <= 255: maintained groups + histogram
   // want_trace (E:192-217): pre_total upkeep for every kind, per-boundary rows
   // and fused J(gamma) counts (sim.py:172-183)
@@ -232,7 +233,7 @@ template <int G, typename Key, typename LeafFn>
 __device__ void group_recompute_list(const TreeRef<Key>& t, const TreeGeom& geo, const int* rec, int n,
                                      const Grp<G>& w, LeafFn leaf) {
   if (G != 32) {
-    for (int i = 0; i < n; ++i) group_recompute(t, geo, rec[i], w, leaf);
+    for (int i = 0; i < n; ++i) group_recompute(t, geo, rec[i] & 0x7fffffff, w, leaf);
     return;
   }
   for (int i0 = 0; i0 < n; i0 += 4) {
@@ -240,7 +241,7 @@ __device__ void group_recompute_list(const TreeRef<Key>& t, const TreeGeom& geo,
     int q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      q[j] = i0 + j < n ? rec[i0 + j] : -1;
+      q[j] = i0 + j < n ? (rec[i0 + j] & 0x7fffffff) : -1;
       k[j] = q[j] >= 0 ? child_key(t, geo, 0, q[j] * 32 + w.lane, leaf) : Key(0);
     }
 #pragma unroll
@@ -261,8 +262,8 @@ __device__ void group_recompute_list(const TreeRef<Key>& t, const TreeGeom& geo,
 // Recompute the ancestors (levels >= 2, shared memory) of the level-1 groups dl[0..n).
 template <int G, typename Key, typename LeafFn>
 __device__ void tree_fix_ancestors(const TreeRef<Key>& t, const TreeGeom& geo, int* dl, int* dl2, int n,
-                                   const Grp<G>& w, LeafFn leaf) {
-  for (int l = 2; l <= geo.levels; ++l) {
+                                   const Grp<G>& w, LeafFn leaf, int l0 = 2) {
+  for (int l = l0; l <= geo.levels; ++l) {
     int cnt = 0;
     for (int base = 0; base < n; base += G) {
       int idx = base + w.lane;
@@ -297,6 +298,55 @@ __device__ void tree_update_list(const TreeRef<Key>& t, const TreeGeom& geo, int
   tree_fix_ancestors(t, geo, dl, dl2, n, w, leaf);
 }
 
+// Level-2 upkeep for a level-1 group q whose max went Q0 -> Qn (rec: to be
+// recomputed from its leaves, new max <= Q0).  A raise is applied at once
+// (atomic max into the shared-memory level-2 node; returns true if it raised
+// it); a recomputed group that held its parent's max flags the parent for a
+// rescan after the recompute (returns hold).  Everything else leaves level 2
+// unchanged -- so the common case (a few groups' maxima move below their
+// parents') costs no child scan and, with level 1 in HBM, no round trip.
+template <typename Key>
+__device__ __forceinline__ bool l2_note(const TreeRef<Key>& t, const TreeGeom& geo, int q, Key Q0, Key Qn, bool rec,
+                                        bool* hold) {
+  *hold = false;
+  if (geo.levels < 2) return false;
+  Key* K2 = t.up + up_off(geo, 2) + (q >> 5);
+  if (rec) {
+    *hold = Q0 == *K2;
+    return false;
+  }
+  if (Qn > Q0) return atomicMax(K2, Qn) < Qn;
+  return false;
+}
+
+// After the level-1 recomputes: rescan the level-2 parents of the flagged
+// (holding) recomputed groups rec[i] (bit 31), append every level-2 node that
+// changed (raised[0..nr) already listed) and fix levels >= 3 above them.
+template <int G, typename Key, typename LeafFn>
+__device__ void l2_finish(const TreeRef<Key>& t, const TreeGeom& geo, const int* rec, int nrec, int* ch, int nch,
+                          int* ch2, const Grp<G>& w, LeafFn leaf) {
+  if (geo.levels < 2) return;
+  Key* K2 = t.up + up_off(geo, 2);
+  for (int i = 0; i < nrec; ++i) {
+    const int r = rec[i];
+    if (r >= 0) continue;  // not a holder
+    const int p = (r & 0x7fffffff) >> 5;
+    int bi;
+    const Key m = w.max_key_only(child_scan<G>(t, geo, 2, p, w.lane, leaf, &bi));
+    const bool chg = m != K2[p];
+    w.sync();
+    if (chg) {
+      if (w.lane == 0) {
+        K2[p] = m;
+        ch[nch] = p;
+      }
+      ++nch;
+    }
+    w.sync();
+  }
+  if (geo.levels > 2 && nch > 0) tree_fix_ancestors(t, geo, ch, ch2, nch, w, leaf, 3);
+}
+
 // Incremental rule for one leaf e of group q getting key kk, applied to the
 // group's (max key Q, argmax I): returns true if the group must be recomputed
 // (its argmax leaf decreased).
@@ -317,15 +367,17 @@ __device__ __forceinline__ bool leaf_rule(Key& Q, int& I, int e, Key kk) {
 // -1, new key kk), lanes of the same group serialised by a match_any leader.
 // Appends groups to recompute to rec[] and changed groups to dirty[].
 template <int G, typename Key>
-__device__ __forceinline__ void apply_leaf_updates(L1Node<Key>* L1, int e, Key kk, const Grp<G>& w, int* se,
-                                                   Key* sk, int* rec, int& nrec, int* dirty, int& ndirty) {
+__device__ __forceinline__ void apply_leaf_updates(const TreeRef<Key>& t, const TreeGeom& geo, int e, Key kk,
+                                                   const Grp<G>& w, int* se, Key* sk, int* rec, int& nrec, int* dirty,
+                                                   int& ndirty) {
+  L1Node<Key>* L1 = t.l1;
   const int q = e >= 0 ? (e >> 5) : -1;
   se[w.lane] = e;
   sk[w.lane] = kk;
   w.sync();
   const unsigned peers = w.match_any(q);
   const bool leader = e >= 0 && (__ffs(peers) - 1) == w.lane;
-  bool r = false, changed = false;
+  bool r = false, changed = false, hold = false;
   if (leader) {
     const L1Node<Key> nd = L1[q];
     Key Q = nd.k;
@@ -344,11 +396,11 @@ __device__ __forceinline__ void apply_leaf_updates(L1Node<Key>* L1, int e, Key k
       o.i = I;
       L1[q] = o;
     }
-    changed = r || Q != Q0;
+    changed = l2_note(t, geo, q, Q0, Q, r, &hold);
   }
   const unsigned rb = w.ballot(r), cb = w.ballot(changed);
-  if (r) rec[nrec + __popc(rb & w.lt)] = q;
-  if (changed) dirty[ndirty + __popc(cb & w.lt)] = q;
+  if (r) rec[nrec + __popc(rb & w.lt)] = hold ? (q | (int)0x80000000) : q;
+  if (changed) dirty[ndirty + __popc(cb & w.lt)] = q >> 5;
   nrec += __popc(rb);
   ndirty += __popc(cb);
   w.sync();
@@ -738,7 +790,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int nrec = 0, ndirty = 0;
     for (int s0 = 0; s0 < nrun; s0 += G) {
       const int si = s0 + lane;
-      bool rec = false, changed = false;
+      bool rec = false, changed = false, hold = false;
       int q = -1;
       if (si < nrun) {
         int a = 0, b = 0;
@@ -785,11 +837,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           o.i = In;
           L1[q] = o;
         }
-        changed = rec || Qn != Q;
+        changed = l2_note(c.rt, geo, q, Q, Qn, rec, &hold);
       }
       const unsigned rb = w.ballot(rec), cb = w.ballot(changed);
-      if (rec) c.dl1[nrec + __popc(rb & w.lt)] = q;
-      if (changed) c.dl0[ndirty + __popc(cb & w.lt)] = q;
+      if (rec) c.dl1[nrec + __popc(rb & w.lt)] = hold ? (q | (int)0x80000000) : q;
+      if (changed) c.dl0[ndirty + __popc(cb & w.lt)] = q >> 5;  // raised level-2 node
       nrec += __popc(rb);
       ndirty += __popc(cb);
     }
@@ -797,7 +849,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     auto rleaf = [&](int e) -> Key { return res_key<T, STORED, G>(c, e); };
     group_recompute_list(c.rt, geo, c.dl1, nrec, w, rleaf);
     w.sync();
-    if (geo.levels > 1) tree_fix_ancestors(c.rt, geo, c.dl0, c.dl1, ndirty, w, rleaf);
+    l2_finish(c.rt, geo, c.dl1, nrec, c.dl0, ndirty, c.dl0 + (geo.levels > 2 ? p.dl_cap : 0), w, rleaf);
   }
   if (CT) {  // incremental CI-tree update: n* first, then the two-hop VNs
     const TreeGeom& geo = p.cgeo;
@@ -805,7 +857,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int* se = (int*)c.stage;  // stage is free again: G (index, key) pairs
     Key* sk = (Key*)(se + 32);
     int nrec = 0, ndirty = 0;
-    apply_leaf_updates(L1, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
+    apply_leaf_updates(c.ct, geo, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
                        c.dl0, ndirty);
     for (int base = 0; base < n_items; base += G) {  // (VN, key) pairs staged by the refresh
       const int t = base + lane;
@@ -815,12 +867,12 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         j = c.cj[t];
         kk = j >= 0 ? c.ck[t] : Key(0);
       }
-      apply_leaf_updates(L1, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
+      apply_leaf_updates(c.ct, geo, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
     }
     auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
     group_recompute_list(c.ct, geo, c.dl1, nrec, w, cleaf);
     w.sync();
-    if (geo.levels > 1) tree_fix_ancestors(c.ct, geo, c.dl0, c.dl1, ndirty, w, cleaf);
+    l2_finish(c.ct, geo, c.dl1, nrec, c.dl0, ndirty, c.dl0 + (geo.levels > 2 ? p.dl_cap : 0), w, cleaf);
   }
   if (MG && p.fast_sel) w.sync();
   c.cnt[C_PROP] += 1;

@@ -260,7 +260,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.so_opre = (int)stake(ci || s->want_trace ? (long long)G->max_items * sizeof(T) : 0);
   p.so_cj = (int)stake(ci || s->want_trace ? (long long)G->max_items * 4 : 0);
   p.so_ck = (int)stake(ct ? (long long)G->max_items * sizeof(Key) : 0);
-  p.so_dl0 = (int)stake(dl * 4);
+  p.dl_cap = (int)dl;
+  p.so_dl0 = (int)stake(2 * dl * 4);  // level-2 change list + its ping-pong partner
   p.so_dl1 = (int)stake(dl * 4);
   p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
   p.so_hist = (int)stake(p.fast_sel ? s->n_g * 4 : 0);
