@@ -379,24 +379,41 @@ __device__ __forceinline__ void apply_leaf_updates(const TreeRef<Key>& t, const 
   const bool leader = e >= 0 && (__ffs(peers) - 1) == w.lane;
   bool r = false, changed = false, hold = false;
   if (leader) {
+    // fold the group's changes (each leaf at most once per call): max new key
+    // mx (lowest leaf mi) and the new key of the argmax leaf I if it changed;
+    // recompute only if I decreased and nothing rose above the old max
     const L1Node<Key> nd = L1[q];
-    Key Q = nd.k;
-    int I = nd.i;
-    const Key Q0 = Q;
-    const int I0 = I;
+    const Key Q = nd.k;
+    const int I = nd.i;
+    Key mx = 0, nI = 0;
+    int mi = 0x7fffffff;
+    bool hasI = false;
     unsigned m = peers;
-    while (m && !r) {
+    while (m) {
       const int s2 = __ffs(m) - 1;
       m &= m - 1;
-      r = leaf_rule(Q, I, se[s2], sk[s2]);
+      const int e2 = se[s2];
+      const Key k2 = sk[s2];
+      if (k2 > mx || (k2 == mx && e2 < mi)) { mx = k2; mi = e2; }
+      if (e2 == I) { hasI = true; nI = k2; }
     }
-    if (!r && (Q != Q0 || I != I0)) {
+    Key Qn = Q;
+    int In = I;
+    if (hasI && nI < Q && !(mx > Q)) {
+      r = true;
+    } else if (mx > Q) {
+      Qn = mx;
+      In = mi;
+    } else if (mx == Q && mi < I) {
+      In = mi;
+    }
+    if (!r && (Qn != Q || In != I)) {
       L1Node<Key> o;
-      o.k = Q;
-      o.i = I;
+      o.k = Qn;
+      o.i = In;
       L1[q] = o;
     }
-    changed = l2_note(t, geo, q, Q0, Q, r, &hold);
+    changed = l2_note(t, geo, q, Q, Qn, r, &hold);
   }
   const unsigned rb = w.ballot(r), cb = w.ballot(changed);
   if (r) rec[nrec + __popc(rb & w.lt)] = hold ? (q | (int)0x80000000) : q;

@@ -314,5 +314,5 @@ def test_fp32_messages_within_1e4_first_1000_updates(code_key, eb, n, kind):
     # early; tests/test_gpu_replay.py compares fp32 values along the
     # reference's own sequence without that limit
     assert compared >= 0.2 * n * 1000, compared
-    if code_key == "C0" and eb >= 6.0:
+    if code_key == "C0" and eb >= 6.0 and kind == "rbp":
         assert sat > 0  # the saturated regime was exercised (|c2v| -> 28.3242)

@@ -52,14 +52,26 @@ def test_replay_f64_matches_reference_stepwise(i, case):
 
 @pytest.mark.parametrize("i,case", CASES)
 def test_replay_state_passes_recompute_audit(i, case):
-    """recompute_all (kernels.py:161-181): residual, totals, pre-totals and CI
-    rebuilt from the messages agree with the GPU's incremental state."""
+    """recompute_all (kernels.py:161-181): totals, pre-totals and CI rebuilt
+    from the message arrays agree with the GPU's incrementally maintained
+    ones.  (Residuals are not audited: the reference's incremental pre_c2v of
+    the other edges of m* is deliberately not refreshed (E:143-144, E:156-157),
+    so |pre - c2v| of the incremental state differs from recompute_all's
+    residual in the reference itself; the GPU reproduces the incremental
+    one, compared in the test above.)"""
+    from tests.util import p0_vec
     spec, g, r = _replay(i, case)
-    res = np.abs(r["pre_c2v"] - r["c2v"])
-    for got, ref in ((res, Z[f"c{i}_a_res"]), (r["total"], Z[f"c{i}_a_total"]),
-                     (r["pre_total"], Z[f"c{i}_a_pretot"])):
-        np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-9)
-    np.testing.assert_allclose(r["ci"], Z[f"c{i}_a_ci"], rtol=1e-6, atol=1e-9)
+    # totals from the C2V messages: the reference's own recompute
+    np.testing.assert_allclose(r["total"], Z[f"c{i}_a_total"], rtol=1e-9, atol=1e-9)
+    # pre-totals and CI from the GPU's own pre_c2v / totals (recompute_all's
+    # formulas, K:175-180): the incremental upkeep is consistent
+    chl = Z[f"c{i}_llrs"].astype(np.float64)
+    for f in range(len(chl)):
+        pt = chl[f].copy()
+        np.add.at(pt, g.edge_vn, r["pre_c2v"][f])
+        np.testing.assert_allclose(r["pre_total"][f], pt, rtol=1e-9, atol=1e-9)
+        ci = np.abs(p0_vec(r["total"][f]) - p0_vec(r["pre_total"][f]))
+        np.testing.assert_allclose(r["ci"][f], ci, rtol=1e-6, atol=1e-12)
 
 
 @pytest.mark.parametrize("i,case", CASES)
