@@ -573,7 +573,13 @@ __device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int 
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
 // pre-C2V (and, for CI schedules, pre_total / CI) state.  Leaves the item
 // table of e* for the LMD searches.
-template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G, bool MG = false, bool TR = false>
+// PF (state in HBM, mode 3 -- BG-sized codes): the two-hop inputs are staged
+// with the V2C loads and the residual-tree level-1 update runs one lane per
+// group run (fewer dependent HBM round trips); with the state in shared memory
+// or L2-sized (modes 0-2) the leaner classic order has fewer live registers
+// and measured faster (C1).
+template <typename T, int KERNEL, bool CI, bool RT, bool CT, bool STORED, int G, bool MG = false, bool TR = false,
+          bool PF = true>
 __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
@@ -585,6 +591,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   // offsets) -> its VN's slots, the committed state, the two-hop items ->
   // the V2C inputs and ALL two-hop inputs / C2V values / pre values together.
   const bool tab = g.hop_items != nullptr;
+  const bool pf = PF && tab;
   int n_items = 0, hsp = 0;
   if (tab) {
     c.items = g.hop_items + g.hop_ptr[e_star];
@@ -603,7 +610,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   const T nv = c.pre[e_star];
   const T tot = c.total[n_star] + (nv - old);  // E:147
   const T cf = act ? c.c2v[adj.x] : T(0);
-  if (tab) {
+  if (pf) {
     // stage the two-hop inputs now: they do not depend on this update's V2C
     // values (items exclude the V2C edges), and keep each item's C2V (and,
     // with pre_total upkeep, its old pre) for the refresh; two items per pass
@@ -693,7 +700,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
   }
   w.sync();
-  if (!tab) {
+  if (!pf) {
     for (int t = lane; t < n_items; t += G) {  // stage the rest of each check
       int4 r = c.items[t];
       c.stage[r.w + (r.x - r.y)] = c.in[r.x];
@@ -711,11 +718,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       const int4 r = c.items[t];
       const int ge = r.x, skip = r.x - r.y;
       // independent loads first (the pre[] store below would otherwise pin them)
-      const T cg = tab ? c.cg[t] : c.c2v[ge];
+      const T cg = pf ? c.cg[t] : c.c2v[ge];
       T opre = T(0);
       if (PT) {
-        j = tab ? c.cj[t] : g.edge_vn[ge];
-        opre = tab ? c.opre[t] : c.pre[ge];
+        j = pf ? c.cj[t] : g.edge_vn[ge];
+        opre = pf ? c.opre[t] : c.pre[ge];
       }
       const T* s = c.stage + r.w;
       T np_;
@@ -785,6 +792,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     // decreased below the new maximum are recomputed from their leaves.
     const TreeGeom& geo = p.rgeo;
     L1Node<Key>* L1 = c.rt.l1;
+    int nrec = 0, ndirty = 0;
+    if (PF) {
     int* segs = (int*)c.stage;  // stage is free again: run starts + sentinel
     const int qs = e_star >> 5;
     int nseg = 0;
@@ -804,7 +813,6 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     w.sync();
     const int nrun = nseg + (covered ? 0 : 1);  // + e*'s group alone
     const Key k0 = Num<T>::key(T(0));
-    int nrec = 0, ndirty = 0;
     for (int s0 = 0; s0 < nrun; s0 += G) {
       const int si = s0 + lane;
       bool rec = false, changed = false, hold = false;
@@ -863,6 +871,73 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       ndirty += __popc(cb);
     }
     w.sync();
+    } else {
+      // classic order: e* first, then one pass per G items (the items of one
+      // group are consecutive), the group's changes folded by a match_any leader
+      const int q = e_star >> 5;
+      const L1Node<Key> nd = L1[q];
+      Key Q = nd.k;
+      int I = nd.i;
+      const Key Q0 = Q;
+      const bool rec = leaf_rule(Q, I, e_star, Num<T>::key(T(0)));
+      bool hold = false;
+      const bool raised = l2_note(c.rt, geo, q, Q0, Q, rec, &hold);
+      w.sync();
+      if (lane == 0) {
+        if (rec) c.dl1[nrec] = hold ? (q | (int)0x80000000) : q;
+        else {
+          L1Node<Key> o;
+          o.k = Q;
+          o.i = I;
+          L1[q] = o;
+        }
+        if (raised) c.dl0[ndirty] = q >> 5;
+      }
+      nrec += rec ? 1 : 0;
+      ndirty += raised ? 1 : 0;
+      w.sync();
+      for (int base = 0; base < n_items; base += G) {
+        const int t = base + lane;
+        const bool valid = t < n_items;
+        const int e = valid ? c.items[t].x : -1;
+        const int qq = valid ? (e >> 5) : -1;
+        const Key kk = valid ? c.nk[t] : Key(0);
+        const unsigned peers = w.match_any(qq);
+        const bool leader = valid && (__ffs(peers) - 1) == lane;
+        Key Qc = 0;
+        int Ic = 0;
+        if (valid) {
+          const L1Node<Key> n2 = L1[qq];
+          Qc = n2.k;
+          Ic = n2.i;
+        }
+        // the group's argmax leaf decreased and nothing rose above the old max -> recompute
+        const bool dec = valid && ((e == Ic && kk < Qc) || p.dbg_full_tree);
+        int bi;
+        const Key km = warp_max_key_minidx_masked(kk, e, peers << w.base, &bi);
+        const bool recq = (w.ballot(dec) & peers) != 0 && !(km > Qc);
+        bool lrec = false, raisedq = false, holdq = false;
+        if (leader) {
+          Key Qn = Qc;
+          if (recq) {
+            lrec = true;
+          } else if (km > Qc || (km == Qc && bi < Ic)) {
+            Qn = km;
+            L1Node<Key> o;
+            o.k = km;
+            o.i = bi;
+            L1[qq] = o;
+          }
+          raisedq = l2_note(c.rt, geo, qq, Qc, Qn, lrec, &holdq);
+        }
+        const unsigned rb = w.ballot(lrec), cb = w.ballot(raisedq);
+        if (lrec) c.dl1[nrec + __popc(rb & w.lt)] = holdq ? (qq | (int)0x80000000) : qq;
+        if (raisedq) c.dl0[ndirty + __popc(cb & w.lt)] = qq >> 5;
+        nrec += __popc(rb);
+        ndirty += __popc(cb);
+        w.sync();
+      }
+    }
     auto rleaf = [&](int e) -> Key { return res_key<T, STORED, G>(c, e); };
     group_recompute_list(c.rt, geo, c.dl1, nrec, w, rleaf);
     w.sync();
@@ -1423,8 +1498,9 @@ __device__ void me_topm_registers(const DynParams& p, Ctx<T, G>& c, int m, LeafF
   c.w.sync();
 }
 
-template <typename T, int KERNEL, int KF, int G, bool TR>
+template <typename T, int KERNEL, int KF, int G, bool TR, int MODE = 3>
 __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
+  constexpr bool PF = MODE == 3;
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
@@ -1458,7 +1534,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       while (c.prop < budget) {
         int e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
         c.cnt[C_CMP] += E - 1;
-        propagate<T, KERNEL, false, true, false, false, G, false, TR>(p, c, e);
+        propagate<T, KERNEL, false, true, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
       }
@@ -1486,8 +1562,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           e = argmax_vn_edges<T, G>(g, c, n_star);
           c.cnt[C_CMP] += g.vrec[n_star].y - 1;
         }
-        if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR>(p, c, e);
-        else propagate<T, KERNEL, true, true, true, false, G, false, TR>(p, c, e);
+        if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR, PF>(p, c, e);
+        else propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (c.prop == c.next_b || c.prop >= budget) {
           if (lane == 0) {
@@ -1505,7 +1581,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       int e = argmax_scan<Key>(g.E, c.w, rleaf);
       c.cnt[C_CMP] += E - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, false, false, false, false, G, false, TR>(p, c, e);
+        int n_items = propagate<T, KERNEL, false, false, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
@@ -1523,7 +1599,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       int e = argmax_vn_edges<T, G>(g, c, n_star);
       c.cnt[C_CMP] += g.vrec[n_star].y - 1;
       while (c.prop < budget) {
-        int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR>(p, c, e);
+        int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
         if (c.prop >= budget) break;
@@ -1545,7 +1621,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int pv = c.sel[idx];
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
-          propagate<T, KERNEL, true, false, false, false, G, true, TR>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
@@ -1561,7 +1637,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           int e = argmax_vn_edges<T, G>(g, c, pv);
           c.cnt[C_CMP] += g.vrec[pv].y - 1;
           if (lane == 0) c.chosen[idx] = e;
-          propagate<T, KERNEL, true, false, false, false, G, true, TR>(p, c, e);
+          propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
@@ -1610,7 +1686,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         c.cnt[C_CMP] += E - 1;
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
-          propagate<T, KERNEL, false, true, false, true, G, false, TR>(p, c, c.sel[idx]);
+          propagate<T, KERNEL, false, true, false, true, G, false, TR, PF>(p, c, c.sel[idx]);
           ++c.prop;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
@@ -1636,7 +1712,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         c.cnt[C_CMP] += E - 1;
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
-          propagate<T, KERNEL, false, true, false, true, G, false, TR>(p, c, c.sel[idx]);
+          propagate<T, KERNEL, false, true, false, true, G, false, TR, PF>(p, c, c.sel[idx]);
           ++c.prop;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
@@ -1722,7 +1798,7 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);
     f = c.w.shfl(f, 0);
     if ((long long)f >= p.B) break;
-    decode_frame<T, KERNEL, KF, G, TR>(p, c, (long long)f);
+    decode_frame<T, KERNEL, KF, G, TR, MODE>(p, c, (long long)f);
   }
 }
 
