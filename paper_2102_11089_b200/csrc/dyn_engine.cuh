@@ -98,6 +98,9 @@ struct DynParams {
   int scratch_bytes;      // per-warp shared scratch
   int so_items, so_stage, so_nk, so_opre, so_cj, so_ck, so_dl0, so_dl1, so_sizes, so_hist;
   int dl_cap;             // entries of dl0 (twice that allocated: ping-pong for the levels >= 3 fix)
+  int me_pairs;           // multi-edge rounds: apply disjoint consecutive VN pairs on the two half-warps
+  int pair_cap;           // ints that fit the stage area (conflict-test buffer)
+  int so_pair;            // scratch offset of the second half-warp's per-update scratch
   int fast_sel;           // ME kinds with n_g <= 255: maintained groups + histogram
   // want_trace (E:192-217): pre_total upkeep for every kind, per-boundary rows
   // and fused J(gamma) counts (sim.py:172-183)
@@ -484,9 +487,10 @@ __device__ int argmax_scan(int n, const Grp<G>& w, KeyFn keyf) {
 
 // E:269-276 -- first maximum residual over M(n) in vn_edges order (= edge order)
 template <typename T, int G>
-__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T, G>& c, int n) {
+__device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T, G>& c, int n, int* deg = nullptr) {
   using Key = typename Num<T>::Key;
   const int2 vr = g.vrec[n];
+  if (deg) *deg = vr.y;  // the caller's comparison count, without reloading vrec
   Key bk = 0;
   int be = 0x7fffffff;
   for (int k = c.lane; k < vr.y; k += G) {  // vn_edges ascend: first max = lowest edge
@@ -1345,9 +1349,10 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T, G>& c, int e_prev, int n
   int best;
   c.w.max_key_minidx(bk, bi, &best);
   if (!simplified) {
+    int dv_ = 0;
     int np_ = g.edge_vn[best];
-    best = argmax_vn_edges<T, G>(g, c, np_);
-    c.cnt[C_CMP] += g.vrec[np_].y - 1;
+    best = argmax_vn_edges<T, G>(g, c, np_, &dv_);
+    c.cnt[C_CMP] += dv_ - 1;
   }
   return best;
 }
@@ -1386,6 +1391,95 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
   int best;
   c.w.max_key_minidx(bk, bj, &best);
   return best;
+}
+
+// ---------------------------------------------- multi-edge round pairing
+// Within a multi-edge round the reference applies the selected VNs one after
+// another in ascending order (E:625-632, SP:407).  Two consecutive VNs a < b
+// touch disjoint state -- so their updates commute exactly, bit for bit --
+// when no VN lies within one check of both, N2(a) ∩ N2(b) = ∅ (N2(v) = the
+// VNs sharing a check with v, v included): then b is not refreshed by a and
+// vice versa (b's residuals, total, CI untouched), they share no check (no
+// V2C / staged input in common) and no pre_total sum receives updates from
+// both (no order-dependent float additions).  Such a pair is applied
+// concurrently, one VN per half-warp; otherwise one after the other.
+template <typename T>
+__device__ bool me_pair_disjoint(const DevGraph& g, Ctx<T, 32>& c, int a, int b, int cap) {
+  const int a0 = g.vn2_ptr[a], la = g.vn2_ptr[a + 1] - a0;
+  const int b0 = g.vn2_ptr[b], lb = g.vn2_ptr[b + 1] - b0;
+  if (la > cap) return false;
+  int* A = (int*)c.stage;  // free between updates
+  for (int t = c.lane; t < la; t += 32) A[t] = g.vn2[a0 + t];
+  c.w.sync();
+  bool hit = false;
+  for (int t = c.lane; t < lb && !hit; t += 32) {
+    const int x = g.vn2[b0 + t];
+    int lo = 0, hi = la;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (A[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    hit = lo < la && A[lo] == x;
+  }
+  const bool any = c.w.any(hit);
+  c.w.sync();
+  return !any;
+}
+
+// The half-warp context of half h: the frame's state and selection state are
+// shared, the per-update scratch is the half's own.
+template <typename T>
+__device__ Ctx<T, 16> half_ctx(const DynParams& p, const Ctx<T, 32>& c, int half) {
+  Ctx<T, 16> h;
+  h.w = Grp<16>::make();
+  h.lane = h.w.lane;
+  h.c2v = c.c2v; h.pre = c.pre; h.in = c.in; h.res = c.res; h.total = c.total; h.pretot = c.pretot;
+  h.ci = c.ci; h.p0t = c.p0t; h.tmp = c.tmp;
+  h.rt = c.rt; h.ct = c.ct;
+  h.inpp = c.inpp; h.gid = c.gid; h.hist = c.hist; h.gbits = c.gbits;
+  h.members = c.members; h.sel = c.sel; h.chosen = c.chosen; h.sizes = c.sizes;
+  const long long d = half ? (long long)(p.so_pair - p.so_items) : 0;
+  auto sh = [&](auto* ptr) { return (decltype(ptr))((unsigned char*)ptr + d); };
+  h.items_buf = sh(c.items_buf);
+  h.items = h.items_buf;
+  h.stage = sh(c.stage);
+  h.nk = sh(c.nk);
+  h.cg = sh(c.cg);
+  h.opre = sh(c.opre);
+  h.cj = sh(c.cj);
+  h.ck = sh(c.ck);
+  h.dl0 = sh(c.dl0);
+  h.dl1 = sh(c.dl1);
+  for (int k = 0; k < kCounters; ++k) h.cnt[k] = 0;
+  h.prop = c.prop + half;
+  h.cur_f = c.cur_f;
+  h.nsel = c.nsel;
+  h.next_b = c.next_b;
+  h.it = c.it;
+  h.rng = c.rng;
+  return h;
+}
+
+// sel[idx] and sel[idx+1] on the two half-warps (CI kinds: E:625-632 per VN)
+template <typename T, int KERNEL, bool TR, bool PF>
+__device__ void me_pair_step(const DynParams& p, Ctx<T, 32>& c, int idx, int* chosen) {
+  const int half = c.lane >> 4;
+  Ctx<T, 16> h = half_ctx<T>(p, c, half);
+  const int pv = c.sel[idx + half];
+  int dv = 0;
+  const int e = argmax_vn_edges<T, 16>(p.g, h, pv, &dv);
+  h.cnt[C_CMP] += dv - 1;
+  if (chosen && h.lane == 0) chosen[idx + half] = e;
+  propagate<T, KERNEL, true, false, false, false, 16, true, TR, PF>(p, h, e);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kCounters; ++k) {
+    long long v = h.cnt[k];
+    v += __shfl_xor_sync(kFull, v, 16);
+    c.cnt[k] += v;
+  }
+  c.prop += 2;
 }
 
 // --------------------------------------------------------------- decoders
@@ -1502,6 +1596,7 @@ template <typename T, int KERNEL, int KF, int G, bool TR, int MODE = 3>
 __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   constexpr bool PF = MODE == 3;
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
+  int dv_ = 0;  // degree of the VN argmax_vn_edges just scanned
   using Key = typename Num<T>::Key;
   const DevGraph& g = p.g;
   const long long E = g.E, budget = (long long)p.i_max * E;
@@ -1559,8 +1654,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
           c.cnt[C_CMP] += E - 1;
         } else {
-          e = argmax_vn_edges<T, G>(g, c, n_star);
-          c.cnt[C_CMP] += g.vrec[n_star].y - 1;
+          e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
+          c.cnt[C_CMP] += dv_ - 1;
         }
         if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR, PF>(p, c, e);
         else propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
@@ -1596,8 +1691,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     case KIND_LMD_CIRBP: {  // E:555-598
       int n_star = argmax_scan<Key>(g.N, c.w, cleaf);
       c.cnt[C_CMP] += g.N - 1;
-      int e = argmax_vn_edges<T, G>(g, c, n_star);
-      c.cnt[C_CMP] += g.vrec[n_star].y - 1;
+      int e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
+      c.cnt[C_CMP] += dv_ - 1;
       while (c.prop < budget) {
         int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
@@ -1608,8 +1703,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           nn = argmax_scan<Key>(g.N, c.w, cleaf);
           c.cnt[C_CMP] += g.N - 1;
         }
-        e = argmax_vn_edges<T, G>(g, c, nn);
-        c.cnt[C_CMP] += g.vrec[nn].y - 1;
+        e = argmax_vn_edges<T, G>(g, c, nn, &dv_);
+        c.cnt[C_CMP] += dv_ - 1;
       }
     } break;
     case KIND_ME_CIRBP: {  // E:601-643
@@ -1617,12 +1712,20 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       while (boundary <= I && !conv) {
         int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
         c.cnt[C_MSEL] += p.n_g;
-        for (int idx = 0; idx < count; ++idx) {
+        for (int idx = 0; idx < count;) {
+          if constexpr (G == 32) {
+            if (p.me_pairs && idx + 1 < count && me_pair_disjoint<T>(g, c, c.sel[idx], c.sel[idx + 1], p.pair_cap)) {
+              me_pair_step<T, KERNEL, TR, PF>(p, c, idx, nullptr);
+              idx += 2;
+              continue;
+            }
+          }
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T, G>(g, c, pv);
-          c.cnt[C_CMP] += g.vrec[pv].y - 1;
+          int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
+          c.cnt[C_CMP] += dv_ - 1;
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
+          ++idx;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
       }
@@ -1632,13 +1735,21 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
       c.cnt[C_MSEL] += p.n_g;
       while (boundary <= I && !conv) {
-        for (int idx = 0; idx < count; ++idx) {
+        for (int idx = 0; idx < count;) {
+          if constexpr (G == 32) {
+            if (p.me_pairs && idx + 1 < count && me_pair_disjoint<T>(g, c, c.sel[idx], c.sel[idx + 1], p.pair_cap)) {
+              me_pair_step<T, KERNEL, TR, PF>(p, c, idx, c.chosen);
+              idx += 2;
+              continue;
+            }
+          }
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T, G>(g, c, pv);
-          c.cnt[C_CMP] += g.vrec[pv].y - 1;
+          int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
+          c.cnt[C_CMP] += dv_ - 1;
           if (lane == 0) c.chosen[idx] = e;
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
+          ++idx;
         }
         me_boundaries<T, G, TR>(p, c, f, &boundary, &conv);
         if (conv || boundary > I) break;

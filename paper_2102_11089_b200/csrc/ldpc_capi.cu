@@ -52,6 +52,7 @@ struct ldpc_graph {
   int* strip_block;
   int* tile_block;
   unsigned char* hop_block;  // precomputed two-hop tables (may be null)
+  int* pair_block;           // per-VN two-hop VN lists (ME round pairing; may be null)
 };
 
 namespace {
@@ -265,6 +266,12 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.so_dl1 = (int)stake(dl * 4);
   p.so_sizes = (int)stake(std::max(1, s->n_g) * 4);
   p.so_hist = (int)stake(p.fast_sel ? s->n_g * 4 : 0);
+  // multi-edge round pairing (dyn_engine.cuh me_pair_step): a second copy of
+  // the per-update scratch [so_items, so_sizes) for the second half-warp
+  p.me_pairs = (s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && G->d.vn2 &&
+               !(s->variant & LDPC_VARIANT_ME_SERIAL) ? 1 : 0;
+  p.pair_cap = (int)((p.so_nk - p.so_stage) / 4);
+  p.so_pair = (int)stake(p.me_pairs ? (long long)(p.so_sizes - p.so_items) : 0);
   p.scratch_bytes = (int)align16(so);
 }
 
@@ -624,7 +631,7 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
   if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
   if (s->want_trace != 0 && s->want_trace != 1) return LDPC_ERR_INVALID;
-  if (s->variant & ~0xff) return LDPC_ERR_INVALID;
+  if (s->variant & ~0x1ff) return LDPC_ERR_INVALID;
   if ((s->variant & LDPC_VARIANT_LANES32) && (s->variant & LDPC_VARIANT_LANES16)) return LDPC_ERR_INVALID;
   if ((s->variant & LDPC_VARIANT_CHECK_TMA) && (s->variant & LDPC_VARIANT_CHECK_LEGACY)) return LDPC_ERR_INVALID;
   return LDPC_OK;
@@ -1148,6 +1155,42 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     G->d.hop_sbptr = (const int*)(hb + o_sbp);
     G->d.hop_sb = (const int*)(hb + o_sb);
   }
+  {  // per-VN sorted two-hop VN sets N2(v) = VNs sharing a check with v (v included),
+     // the conflict test of multi-edge rounds (dyn_engine.cuh me_pair_disjoint); <= 64 MB
+    std::vector<int> v2ptr(N + 1, 0), v2, stamp(N, -1), tmp;
+    bool ok = true;
+    for (int v = 0; v < N && ok; ++v) {
+      tmp.clear();
+      for (int k = vn_ptr[v]; k < vn_ptr[v + 1]; ++k) {
+        const int i = edge_cn[vn_edges[k]];
+        for (int g2 = cn_ptr[i]; g2 < cn_ptr[i + 1]; ++g2) {
+          const int j = edge_vn[g2];
+          if (stamp[j] != v) {
+            stamp[j] = v;
+            tmp.push_back(j);
+          }
+        }
+      }
+      if (tmp.empty()) tmp.push_back(v);
+      std::sort(tmp.begin(), tmp.end());
+      v2.insert(v2.end(), tmp.begin(), tmp.end());
+      v2ptr[v + 1] = (int)v2.size();
+      ok = v2.size() <= (16u << 20);
+    }
+    G->pair_block = nullptr;
+    if (ok) {
+      int* pb = nullptr;
+      if (cudaMalloc(&pb, (v2ptr.size() + v2.size()) * sizeof(int)) == cudaSuccess &&
+          cudaMemcpy(pb, v2ptr.data(), v2ptr.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+          cudaMemcpy(pb + v2ptr.size(), v2.data(), v2.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess) {
+        G->pair_block = pb;
+        G->d.vn2_ptr = pb;
+        G->d.vn2 = pb + v2ptr.size();
+      } else if (pb) {
+        cudaFree(pb);
+      }
+    }
+  }
   G->dev_block = d;
   G->max_dv = max_dv;
   G->min_dv = N > 0 ? 1 << 30 : 0;
@@ -1186,6 +1229,7 @@ int ldpc_graph_destroy(ldpc_graph_t* G) {
   cudaFree(G->tile_block);
   cudaFree(G->strip_block);
   if (G->hop_block) cudaFree(G->hop_block);
+  if (G->pair_block) cudaFree(G->pair_block);
   delete G;
   return LDPC_OK;
 }

@@ -48,6 +48,9 @@ struct DevGraph {
   const int4* hop_items;    // item records (g, check start, check degree, stage base)
   const int* hop_sbptr;     // [E]  offset of e's per-VN-slot stage bases in hop_sb
   const int* hop_sb;        // stage base of each vn_edges slot of vn(e) (-1 for cn(e))
+  // optional per-VN two-hop VN sets (sorted; null when too large): ME round pairing
+  const int* vn2_ptr;       // [N+1]
+  const int* vn2;           // N2(v) = VNs sharing a check with v, v included
 };
 
 // 32-ary max-tree geometry over `n` leaves (levels 1..L; level L has <= 64 nodes,
