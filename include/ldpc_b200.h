@@ -91,7 +91,8 @@ typedef struct {
 #define LDPC_VARIANT_LANES32 0x20      /* dynamic: 32 lanes per frame */
 #define LDPC_VARIANT_LANES16 0x40      /* dynamic: 16 lanes per frame (2 frames per warp) */
 #define LDPC_VARIANT_FULL_TREE 0x80    /* dynamic (debug): recompute every touched tree group */
-#define LDPC_VARIANT_ME_SERIAL 0x100   /* multi-edge rounds strictly one VN at a time (no pairing) */
+#define LDPC_VARIANT_ME_PAIRS 0x100    /* multi-edge rounds: disjoint consecutive VN pairs on the two
+                                          half-warps (exact; measured slower: the halves diverge) */
 
 /* Build the device-resident Tanner graph (edge ids in (check, vn) order,
  * vn_edges = stable argsort of edge_vn).  Replaces build_tanner's arrays

@@ -29,7 +29,7 @@ class LdpcSched(C.Structure):
 # ldpc_sched_t.variant bits (include/ldpc_b200.h)
 VARIANTS = {"fixed_phase": 0x1, "fixed_tile": 0x2, "fixed_pipe": 0x3, "check_tma": 0x4,
             "check_legacy": 0x8, "no_layered_sign": 0x10, "lanes32": 0x20, "lanes16": 0x40,
-            "full_tree": 0x80, "me_serial": 0x100}
+            "full_tree": 0x80, "me_pairs": 0x100}
 
 
 def variant_bits(names):

@@ -1403,6 +1403,10 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
 // V2C / staged input in common) and no pre_total sum receives updates from
 // both (no order-dependent float additions).  Such a pair is applied
 // concurrently, one VN per half-warp; otherwise one after the other.
+// Opt-in (LDPC_VARIANT_ME_PAIRS): exact, but measured 2x slower on C1
+// ME-CIRBP(4) and 1.5x on C3 ME-CIRBP(64) -- the two half-warps run different
+// data through data-dependent loops, diverge and serialise, and the conflict
+// test costs two extra dependent loads per pair.
 template <typename T>
 __device__ bool me_pair_disjoint(const DevGraph& g, Ctx<T, 32>& c, int a, int b, int cap) {
   const int a0 = g.vn2_ptr[a], la = g.vn2_ptr[a + 1] - a0;

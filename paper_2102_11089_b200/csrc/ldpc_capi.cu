@@ -269,7 +269,7 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   // multi-edge round pairing (dyn_engine.cuh me_pair_step): a second copy of
   // the per-update scratch [so_items, so_sizes) for the second half-warp
   p.me_pairs = (s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && G->d.vn2 &&
-               !(s->variant & LDPC_VARIANT_ME_SERIAL) ? 1 : 0;
+               (s->variant & LDPC_VARIANT_ME_PAIRS) ? 1 : 0;
   p.pair_cap = (int)((p.so_nk - p.so_stage) / 4);
   p.so_pair = (int)stake(p.me_pairs ? (long long)(p.so_sizes - p.so_items) : 0);
   p.scratch_bytes = (int)align16(so);

@@ -69,12 +69,12 @@ def test_variant_bits_validated():
 @pytest.mark.parametrize("kind", ["me_cirbp", "me_lmd_cirbp"])
 def test_me_round_pairing_is_exact(code_key, eb, i_max, count, n_p, kind):
     """Multi-edge rounds with disjoint consecutive VN pairs applied on the two
-    half-warps == strictly one VN at a time (ldpc_sched_t.variant ME_SERIAL):
+    half-warps (ldpc_sched_t.variant ME_PAIRS) == strictly one VN at a time:
     every output bit-identical (the reference's sequential order, E:625-632)."""
     spec, g = load_code(code_key)
     llrs = torch.from_numpy(llr_batch(spec, eb, seed=8, start=0, count=count)).cuda()
     cfg = ScheduleConfig(kind=kind, i_max=i_max, n_p=n_p)
-    a = results_to_numpy(decode_batch(spec, llrs, cfg), kind, i_max)
-    b = results_to_numpy(decode_batch(spec, llrs, cfg, variant="me_serial"), kind, i_max)
+    a = results_to_numpy(decode_batch(spec, llrs, cfg, variant="me_pairs"), kind, i_max)
+    b = results_to_numpy(decode_batch(spec, llrs, cfg), kind, i_max)
     for key in ("u_hat", "prop", "converged", "counters", "bit_errors_at", "info_bit_errors_at"):
         np.testing.assert_array_equal(a[key], b[key], err_msg=key)
