@@ -238,8 +238,7 @@ def cpu_baseline(wl, spec, g, llr_host, gpu_outs, budget_s=20.0):
             per[_sname(kind, n_p)] = {"updates_per_s": u / (time.perf_counter() - t1),
                                       "frame_errors": int((r["bit_errors_at"][:, -1] > 0).sum()),
                                       "bit_errors": int(r["info_bit_errors_at"][:, -1].sum()),
-                                      "bits_mean": float(r["info_bit_errors_at"][:, -1].mean()),
-                                      "bits_sd": float(r["info_bit_errors_at"][:, -1].std(ddof=1)) if n > 1 else 0.0,
+                                      "bits": r["info_bit_errors_at"][:, -1].copy(),
                                       "frames": n, "identical": int(same.sum())}
             tot_u += u
         return tot_u, time.perf_counter() - t0, per
@@ -254,7 +253,7 @@ def cpu_baseline(wl, spec, g, llr_host, gpu_outs, budget_s=20.0):
             "frames_per_s": n * len(scheds) / t,
             "per_schedule_updates_per_s": {k: v["updates_per_s"] for k, v in per.items()},
             "per_schedule_fer": {k: (v["frame_errors"], v["frames"]) for k, v in per.items()},
-            "per_schedule_info_bits": {k: (v["bits_mean"], v["bits_sd"], v["frames"]) for k, v in per.items()},
+            "per_schedule_info_bits": {k: v["bits"] for k, v in per.items()},
             "gpu_oracle_identical": {k: [v["identical"], v["frames"]] for k, v in per.items()}}
 
 
@@ -282,6 +281,22 @@ def cpu_reference(wl, spec, llr_host, budget_s=30.0):
                       f"ldpc_ids.schedules.decode (numba) on a {cores}-process pool ({t:.1f} s)",
             "per_schedule_updates_per_s": {_sname(k, m): v[0] / t * len(r) for (k, m), v in r.items()},
             "per_schedule_fer": {_sname(k, m): (v[1], n) for (k, m), v in r.items()}}
+
+
+def ber_ci(bits_per_frame, k_info, alpha=0.05, reps=2000, seed=0):
+    """95 % interval of the info-bit error rate from per-frame bit-error counts:
+    percentile bootstrap over frames (bit errors cluster in erroneous frames,
+    so a binomial over bits would be far too narrow)."""
+    b = np.asarray(bits_per_frame, np.float64)
+    n = len(b)
+    if n == 0:
+        return 0.0, 1.0
+    rng = np.random.default_rng(seed)
+    means = b[rng.integers(0, n, size=(reps, n))].mean(1)
+    lo, hi = np.quantile(means, [alpha / 2, 1 - alpha / 2])
+    if b.sum() == 0:  # no error in the sample: BER <= FER <= 3/n (rule of three)
+        return 0.0, 3.0 / n
+    return float(lo) / k_info, float(hi) / k_info
 
 
 def clopper_pearson(k, n, alpha=0.05):
@@ -464,13 +479,12 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
                 per[nm]["oracle_fer_sample"] = k / n
                 per[nm]["oracle_fer_ci95"] = [lo, hi]
                 per[nm]["fer_inside_oracle_ci95"] = bool(lo <= per[nm]["fer"] <= hi)
-        # BER (info bits): normal CI over the sample's per-frame bit-error counts
-        for nm, (bits_mean, bits_sd, n) in cb["per_schedule_info_bits"].items():
+        # BER (info bits): frame-level bootstrap interval of the sample's rate
+        for nm, bits in cb["per_schedule_info_bits"].items():
             if nm in per:
                 k = max(1, spec.k_info)
-                half = 1.96 * bits_sd / max(1, n) ** 0.5
-                lo, hi = max(0.0, (bits_mean - half) / k), (bits_mean + half) / k
-                per[nm]["oracle_ber_sample"] = bits_mean / k
+                lo, hi = ber_ci(bits, k)
+                per[nm]["oracle_ber_sample"] = float(np.mean(bits)) / k
                 per[nm]["oracle_ber_ci95"] = [lo, hi]
                 per[nm]["ber_inside_oracle_ci95"] = bool(lo <= per[nm]["ber_info"] <= hi)
     return line

@@ -126,7 +126,7 @@ struct Ctx {
   T* cg;          // C2V of each item, staged with its inputs (aliases nk: read before nk is written)
   T* opre;        // old pre of each item (pre_total upkeep)
   int* cj;        // VN of each item (pre_total upkeep; -1: not its last occurrence)
-  Key* ck;        // CI key of each item's VN after the refresh (CI tree)
+  Key* ck;        // CI key of each item's VN after the refresh (CI tree; aliases opre, read first)
   int *dl0, *dl1; // dirty-node lists for tree maintenance
   int* sizes;     // Alg.4 group histogram
   long long cnt[kCounters];

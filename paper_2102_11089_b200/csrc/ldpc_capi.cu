@@ -260,7 +260,7 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.so_nk = (int)stake((long long)G->max_items * std::max(sizeof(Key), sizeof(T)));  // keys; staged C2V values
   p.so_opre = (int)stake(ci || s->want_trace ? (long long)G->max_items * sizeof(T) : 0);
   p.so_cj = (int)stake(ci || s->want_trace ? (long long)G->max_items * 4 : 0);
-  p.so_ck = (int)stake(ct ? (long long)G->max_items * sizeof(Key) : 0);
+  p.so_ck = p.so_opre;  // CI keys overwrite each item's old pre once the refresh has read it
   p.dl_cap = (int)dl;
   p.so_dl0 = (int)stake(2 * dl * 4);  // level-2 change list + its ping-pong partner
   p.so_dl1 = (int)stake(dl * 4);
@@ -311,11 +311,20 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
     if (per > optin) return c;
     void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16, s->want_trace);
     if (!fn) return c;
-    int w = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / std::max<long long>(per, 1));
-    c.wpb = std::max(1, w);
-    c.smem = per * c.wpb;
-    c.occ = dyn_occupancy<T>(fn, c.wpb, (int)c.smem);
-    c.frames = std::min<long long>((long long)c.occ * c.wpb * fpw * sm_count(), B);
+    // warps per block: the size (<= 8) that leaves the most frames resident
+    // (shared memory per SM is allocated in whole blocks)
+    const int wmax = per > 32 * 1024 ? 1 : (int)std::min<long long>(8, optin / std::max<long long>(per, 1));
+    for (int w = std::max(1, wmax); w >= 1; w = w > 2 ? w / 2 : w - 1) {
+      const long long sm = per * w;
+      const int occ = dyn_occupancy<T>(fn, w, (int)sm);
+      const long long fr = std::min<long long>((long long)occ * w * fpw * sm_count(), B);
+      if (fr > c.frames) {
+        c.wpb = w;
+        c.smem = sm;
+        c.occ = occ;
+        c.frames = fr;
+      }
+    }
     return c;
   };
   std::vector<Cand> cands;
@@ -708,6 +717,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.tr = tr;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
     void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16, s->want_trace);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
     void* args[] = {&p};
     if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,
                                              pl.smem_bytes, st)))
