@@ -299,6 +299,15 @@ def ber_ci(bits_per_frame, k_info, alpha=0.05, reps=2000, seed=0):
     return float(lo) / k_info, float(hi) / k_info
 
 
+def _json_default(o):
+    """numpy scalars / arrays that reach the JSON line as plain Python values."""
+    if isinstance(o, np.ndarray):
+        return o.tolist()
+    if isinstance(o, np.generic):
+        return o.item()
+    raise TypeError(f"Object of type {o.__class__.__name__} is not JSON serializable")
+
+
 def clopper_pearson(k, n, alpha=0.05):
     """Exact two-sided binomial confidence interval (FER CI, north star)."""
     from scipy.stats import beta
@@ -318,7 +327,7 @@ def run_ours(args, wl):
         sec = measure(args, WORKLOADS["C3"], "C3", 1, 1, rank, world, local, batch=0, cpu=cpu, e2e=False)
         line["secondary"] = {"C3": {k: sec[k] for k in sec if k not in ("e2e",)}}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=_json_default), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -480,7 +489,7 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
                 per[nm]["oracle_fer_ci95"] = [lo, hi]
                 per[nm]["fer_inside_oracle_ci95"] = bool(lo <= per[nm]["fer"] <= hi)
         # BER (info bits): frame-level bootstrap interval of the sample's rate
-        for nm, bits in cb["per_schedule_info_bits"].items():
+        for nm, bits in cb.pop("per_schedule_info_bits").items():
             if nm in per:
                 k = max(1, spec.k_info)
                 lo, hi = ber_ci(bits, k)
