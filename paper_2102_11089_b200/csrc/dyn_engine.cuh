@@ -129,7 +129,7 @@ struct Ctx {
   Key* ck;        // CI key of each item's VN after the refresh (CI tree; aliases opre, read first)
   int *dl0, *dl1; // dirty-node lists for tree maintenance
   int* sizes;     // Alg.4 group histogram
-  long long cnt[kCounters];
+  long long cnt;     // work counters (E:17-25), one per lane: lane k holds counter k
   long long prop;
   long long cur_f;   // frame being decoded
   int nsel;          // Alg.-4 selections made (debug log index)
@@ -137,6 +137,9 @@ struct Ctx {
   int it;            // completed iterations
   int lane;          // lane within the group (= w.lane)
   long long rng;
+  __device__ __forceinline__ void count(int k, long long v) {
+    if (lane == k) cnt += v;
+  }
 };
 
 // residual leaf key: |pre - c2v| (or the stored residual for ME-RBP's exclusion)
@@ -613,6 +616,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   const T old = c.c2v[e_star];
   const T nv = c.pre[e_star];
   const T tot = c.total[n_star] + (nv - old);  // E:147
+  T ptn = T(0);  // pre_total of n* (unchanged by this update: the items exclude n*'s edges)
+  if (CI) ptn = c.pretot[n_star];
   const T cf = act ? c.c2v[adj.x] : T(0);
   if (pf) {
     // stage the two-hop inputs now: they do not depend on this update's V2C
@@ -668,14 +673,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     c.c2v[e_star] = nv;
     if (STORED) c.res[e_star] = T(0);
-    c.total[n_star] = tot;
-    if (CI) {
-      const T pt = p0_cache(tot);  // cached p0(total) of n*, the only total that changes
-      c.p0t[n_star] = pt;
-      const T cv = ci_cached(pt, c.pretot[n_star]);  // E:148-149
-      c.ci[n_star] = cv;
-      if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
-    }
+    c.total[n_star] = tot;  // n*'s own CI (E:148-149) is evaluated on spare lanes of the refresh below
   }
   // V2C to the other checks of n* (E:153-160), also staged; slots in chunks of G
   int ci_ = 0, cs_ = 0;
@@ -712,10 +710,18 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     w.sync();
   }
   const bool dup = PT && g.hop_dup[e_star] != 0;
+  // n*'s own CI (E:148-149: its total changed, its pre_total did not) rides on
+  // spare lanes of the refresh -- kSelf pseudo-items right after the real ones
+  // (kept inside one pass) -- so no lane evaluates an exp/division chain alone.
+  constexpr int kSelf = CI ? CiSplit<T>::kSelfLanes : 0;
+  int ps0 = n_items;
+  if (kSelf == 2 && (ps0 & (G - 1)) == G - 1) ++ps0;
+  const int n_loop = CI ? ps0 + kSelf : n_items;
   // two-hop refresh (E:161-176), G edges per pass in reference order
-  for (int base = 0; base < n_items; base += G) {
+  for (int base = 0; base < n_loop; base += G) {
     const int t = base + lane;
     const bool valid = t < n_items;
+    const bool self = CI && t >= ps0 && t < ps0 + kSelf;
     int j = -1;
     T delta = T(0);
     if (valid) {
@@ -752,18 +758,16 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       if (RT) c.nk[t] = Num<T>::key(rv);
     }
     if (PT) {
+      bool want = false;  // this lane evaluates a CI: (cache, x) -> probe
+      T cache = T(0), x = T(0);
       if (!dup) {
         if (valid) {
-          T pt = c.pretot[j] + delta;  // E:171
-          c.pretot[j] = pt;
+          x = c.pretot[j] + delta;  // E:171
+          c.pretot[j] = x;
           if (CI) {
-            const T cv = ci_cached(c.p0t[j], pt);  // E:173 (p0(total[j]) cached)
-            c.ci[j] = cv;
-            if (CT) {  // (VN, CI key) of this item for the CI-tree update
-              c.cj[t] = j;
-              c.ck[t] = Num<T>::key(cv);
-            }
-            if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+            cache = c.p0t[j];  // E:173 (p0(total[j]) cached)
+            want = true;
+            if (CT) c.cj[t] = j;
           }
         }
       } else {
@@ -777,12 +781,32 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         }
         const bool last = valid && ((peers >> lane) >> 1) == 0;
         if (CI && last) {
-          const T cv = ci_cached(c.p0t[j], c.pretot[j]);
+          x = c.pretot[j];
+          cache = c.p0t[j];
+          want = true;
+        }
+        if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
+      }
+      if (CI) {
+        if (self) {  // n*: float64 lanes (p0(total), p0(pre_total)); float32 one lane
+          x = (kSelf == 2 && t == ps0) ? tot : ptn;
+          cache = tot;
+        }
+        T pr = T(0);
+        if (want || self) pr = CiSplit<T>::probe(cache, x);
+        T pr_next = T(0);
+        if (kSelf == 2) pr_next = w.shfl_down(pr, 1);
+        if (want) {
+          const T cv = CiSplit<T>::join(cache, pr);
           c.ci[j] = cv;
           if (CT) c.ck[t] = Num<T>::key(cv);
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+        } else if (self && t == ps0) {
+          const T cv = kSelf == 2 ? Num<T>::abs_(pr - pr_next) : pr;
+          c.p0t[n_star] = kSelf == 2 ? pr : tot;  // p0_cache(total[n*])
+          c.ci[n_star] = cv;
+          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
         }
-        if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
       }
     }
   }
@@ -971,10 +995,10 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     l2_finish(c.ct, geo, c.dl1, nrec, c.dl0, ndirty, c.dl0 + (geo.levels > 2 ? p.dl_cap : 0), w, cleaf);
   }
   if (MG && p.fast_sel) w.sync();
-  c.cnt[C_PROP] += 1;
-  c.cnt[C_V2C] += vr.y - 1;
-  c.cnt[C_PRE] += n_items;
-  if (CI) c.cnt[C_CI] += n_items;
+  c.count(C_PROP, 1);
+  c.count(C_V2C, vr.y - 1);
+  c.count(C_PRE, n_items);
+  if (CI) c.count(C_CI, n_items);
   return n_items;
 }
 
@@ -1344,7 +1368,7 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T, G>& c, int e_prev, int n
       if (k > bk) { bk = k; bi = e; }
     }
   }
-  if (ncand > 1) c.cnt[C_CMP] += ncand - 1;
+  if (ncand > 1) c.count(C_CMP, ncand - 1);
   if (ncand <= 0) return -1;
   int best;
   c.w.max_key_minidx(bk, bi, &best);
@@ -1352,7 +1376,7 @@ __device__ int lmd_next_edge(const DynParams& p, Ctx<T, G>& c, int e_prev, int n
     int dv_ = 0;
     int np_ = g.edge_vn[best];
     best = argmax_vn_edges<T, G>(g, c, np_, &dv_);
-    c.cnt[C_CMP] += dv_ - 1;
+    c.count(C_CMP, dv_ - 1);
   }
   return best;
 }
@@ -1386,7 +1410,7 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
       if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
     }
   }
-  if (ncand > 1) c.cnt[C_CMP] += ncand - 1;
+  if (ncand > 1) c.count(C_CMP, ncand - 1);
   if (ncand <= 0) return -1;
   int best;
   c.w.max_key_minidx(bk, bj, &best);
@@ -1455,7 +1479,7 @@ __device__ Ctx<T, 16> half_ctx(const DynParams& p, const Ctx<T, 32>& c, int half
   h.ck = sh(c.ck);
   h.dl0 = sh(c.dl0);
   h.dl1 = sh(c.dl1);
-  for (int k = 0; k < kCounters; ++k) h.cnt[k] = 0;
+  h.cnt = 0;
   h.prop = c.prop + half;
   h.cur_f = c.cur_f;
   h.nsel = c.nsel;
@@ -1473,16 +1497,12 @@ __device__ void me_pair_step(const DynParams& p, Ctx<T, 32>& c, int idx, int* ch
   const int pv = c.sel[idx + half];
   int dv = 0;
   const int e = argmax_vn_edges<T, 16>(p.g, h, pv, &dv);
-  h.cnt[C_CMP] += dv - 1;
+  h.count(C_CMP, dv - 1);
   if (chosen && h.lane == 0) chosen[idx + half] = e;
   propagate<T, KERNEL, true, false, false, false, 16, true, TR, PF>(p, h, e);
   __syncwarp();
-#pragma unroll
-  for (int k = 0; k < kCounters; ++k) {
-    long long v = h.cnt[k];
-    v += __shfl_xor_sync(kFull, v, 16);
-    c.cnt[k] += v;
-  }
+  // half lane k holds counter k of its half: full-warp lanes k < 8 collect both
+  c.cnt += h.cnt + __shfl_xor_sync(kFull, h.cnt, 16);
   c.prop += 2;
 }
 
@@ -1605,7 +1625,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   const DevGraph& g = p.g;
   const long long E = g.E, budget = (long long)p.i_max * E;
   const int lane = c.lane, I = p.i_max;
-  for (int k = 0; k < kCounters; ++k) c.cnt[k] = 0;
+  c.cnt = 0;
   c.prop = 0;
   c.cur_f = f;
   c.nsel = 0;
@@ -1632,7 +1652,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       tree_build(c.rt, p.rgeo, c.w, rleaf);
       while (c.prop < budget) {
         int e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
-        c.cnt[C_CMP] += E - 1;
+        c.count(C_CMP, E - 1);
         propagate<T, KERNEL, false, true, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (single_boundary<T, G, TR>(p, c, f, &conv)) break;
@@ -1647,19 +1667,19 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       while (c.prop < budget) {
         const int it = c.it;
         int n_star = flat ? argmax_scan<Key>(g.N, c.w, cleaf) : tree_argmax(c.ct, p.cgeo, c.w, cleaf);
-        c.cnt[C_CMP] += g.N - 1 + 1;
-        c.cnt[C_KTRIALS] += 1;
+        c.count(C_CMP, g.N - 1 + 1);
+        c.count(C_KTRIALS, 1);
         ++kt;
         bool hit = c.ci[n_star] < gamma;
         int e;
         if (hit) {
-          c.cnt[C_KHITS] += 1;
+          c.count(C_KHITS, 1);
           ++kh;
           e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
-          c.cnt[C_CMP] += E - 1;
+          c.count(C_CMP, E - 1);
         } else {
           e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
-          c.cnt[C_CMP] += dv_ - 1;
+          c.count(C_CMP, dv_ - 1);
         }
         if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR, PF>(p, c, e);
         else propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
@@ -1678,7 +1698,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     case KIND_SLMDRBP: {  // E:472-510
       const bool simplified = p.kind == KIND_SLMDRBP;  // sLMDRBP runs the LMDRBP kernel
       int e = argmax_scan<Key>(g.E, c.w, rleaf);
-      c.cnt[C_CMP] += E - 1;
+      c.count(C_CMP, E - 1);
       while (c.prop < budget) {
         int n_items = propagate<T, KERNEL, false, false, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
@@ -1687,16 +1707,16 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         int en = lmd_next_edge<T, G>(p, c, e, n_items, simplified);
         if (en < 0) {
           en = argmax_scan<Key>(g.E, c.w, rleaf);
-          c.cnt[C_CMP] += E - 1;
+          c.count(C_CMP, E - 1);
         }
         e = en;
       }
     } break;
     case KIND_LMD_CIRBP: {  // E:555-598
       int n_star = argmax_scan<Key>(g.N, c.w, cleaf);
-      c.cnt[C_CMP] += g.N - 1;
+      c.count(C_CMP, g.N - 1);
       int e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
-      c.cnt[C_CMP] += dv_ - 1;
+      c.count(C_CMP, dv_ - 1);
       while (c.prop < budget) {
         int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
@@ -1705,17 +1725,17 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         int nn = ci_argmax_twohop<T, G>(p, c, e, n_items, true);
         if (nn < 0) {
           nn = argmax_scan<Key>(g.N, c.w, cleaf);
-          c.cnt[C_CMP] += g.N - 1;
+          c.count(C_CMP, g.N - 1);
         }
         e = argmax_vn_edges<T, G>(g, c, nn, &dv_);
-        c.cnt[C_CMP] += dv_ - 1;
+        c.count(C_CMP, dv_ - 1);
       }
     } break;
     case KIND_ME_CIRBP: {  // E:601-643
       int boundary = 1;
       while (boundary <= I && !conv) {
         int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
-        c.cnt[C_MSEL] += p.n_g;
+        c.count(C_MSEL, p.n_g);
         for (int idx = 0; idx < count;) {
           if constexpr (G == 32) {
             if (p.me_pairs && idx + 1 < count && me_pair_disjoint<T>(g, c, c.sel[idx], c.sel[idx + 1], p.pair_cap)) {
@@ -1726,7 +1746,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           }
           int pv = c.sel[idx];
           int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
-          c.cnt[C_CMP] += dv_ - 1;
+          c.count(C_CMP, dv_ - 1);
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
           ++idx;
@@ -1737,7 +1757,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     case KIND_ME_LMD_CIRBP: {  // E:646-716
       int boundary = 1;
       int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
-      c.cnt[C_MSEL] += p.n_g;
+      c.count(C_MSEL, p.n_g);
       while (boundary <= I && !conv) {
         for (int idx = 0; idx < count;) {
           if constexpr (G == 32) {
@@ -1749,7 +1769,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           }
           int pv = c.sel[idx];
           int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
-          c.cnt[C_CMP] += dv_ - 1;
+          c.count(C_CMP, dv_ - 1);
           if (lane == 0) c.chosen[idx] = e;
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
@@ -1774,7 +1794,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         }
         if (npc < p.n_p) {
           int extra = select_vns<T, G>(p, c, c.inpp, p.n_p - npc, c.sel + npc);
-          c.cnt[C_MSEL] += p.n_g;
+          c.count(C_MSEL, p.n_g);
           count = npc + extra;
         } else {
           count = npc;
@@ -1798,7 +1818,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       const bool reg_topm = G == 32 && p.rgeo.levels == 1 && np_ <= 4;
       while (boundary <= I && !conv && reg_topm) {
         me_topm_registers<T, G>(p, c, np_, sleaf);
-        c.cnt[C_CMP] += E - 1;
+        c.count(C_CMP, E - 1);
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
           propagate<T, KERNEL, false, true, false, true, G, false, TR, PF>(p, c, c.sel[idx]);
@@ -1824,7 +1844,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         }
         c.w.sync();
         tree_update_list(c.rt, p.rgeo, c.dl0, c.dl1, np_, c.w, sleaf);
-        c.cnt[C_CMP] += E - 1;
+        c.count(C_CMP, E - 1);
         sort_small<T, G>(c, c.sel, np_);
         for (int idx = 0; idx < np_; ++idx) {
           propagate<T, KERNEL, false, true, false, true, G, false, TR, PF>(p, c, c.sel[idx]);
@@ -1838,13 +1858,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   }
   if (I == 0) conv = syndrome_ok<T, G>(g, c.total, c.w);  // schedules.py:144-146
   for (int n = lane; n < g.N; n += G) p.u_hat[f * g.N + n] = c.total[n] < T(0) ? 1 : 0;
-  if (lane < kCounters) {
-    long long v = 0;
-#pragma unroll
-    for (int k = 0; k < kCounters; ++k)
-      if (k == lane) v = c.cnt[k];
-    p.counters[f * kCounters + lane] = v;
-  }
+  if (lane < kCounters) p.counters[f * kCounters + lane] = c.cnt;
   if (lane == 0) {
     p.prop[f] = c.prop;
     p.conv[f] = conv ? 1 : 0;
@@ -1974,7 +1988,7 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   c.dl1 = (int*)(scr + p.so_dl1);
   c.sizes = (int*)(scr + p.so_sizes);
   c.hist = (int*)(scr + p.so_hist);
-  for (int k = 0; k < kCounters; ++k) c.cnt[k] = 0;
+  c.cnt = 0;
   c.prop = 0;
   c.cur_f = f;
   c.nsel = 0;
@@ -1999,13 +2013,7 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
     o[2 * g.E + g.N + n] = (double)c.pretot[n];
     o[2 * g.E + 2 * g.N + n] = (double)c.ci[n];
   }
-  if (c.lane < kCounters) {
-    long long v = 0;
-#pragma unroll
-    for (int k = 0; k < kCounters; ++k)
-      if (k == c.lane) v = c.cnt[k];
-    p.counters[f * kCounters + c.lane] = v;
-  }
+  if (c.lane < kCounters) p.counters[f * kCounters + c.lane] = c.cnt;
 }
 
 }  // namespace ldpc

@@ -128,10 +128,13 @@ template <typename T> __device__ __forceinline__ T clampv(T x) {  // E:31-37
   return x;
 }
 
-template <typename T> __device__ __forceinline__ T p0(T llr) {  // E:40-46
-  if (llr >= T(0)) return T(1) / (T(1) + Num<T>::exp_(-llr));
-  T e = Num<T>::exp_(llr);
-  return e / (T(1) + e);
+// E:40-46: llr >= 0 ? 1 / (1 + exp(-llr)) : exp(llr) / (1 + exp(llr)).  Both
+// branches take the same exponential, exp(-|llr|), so one evaluation and one
+// division give the reference's value bit for bit -- without the divergent
+// double evaluation when a warp holds both signs.
+template <typename T> __device__ __forceinline__ T p0(T llr) {
+  const T e = Num<T>::exp_(-Num<T>::abs_(llr));
+  return (llr >= T(0) ? T(1) : e) / (T(1) + e);
 }
 
 template <typename T> __device__ __forceinline__ T ci_of(T tot, T pre_tot) {
@@ -151,6 +154,24 @@ template <typename T> __device__ __forceinline__ T ci_cached(T cache, T pre_tot)
 template <> __device__ __forceinline__ float ci_cached<float>(float tot, float pre_tot) {
   return p0(tot) * p0(-pre_tot) * fabsf(expm1f(pre_tot - tot));
 }
+
+// CI evaluation split for the two-hop refresh (dyn_engine.cuh propagate): every
+// lane evaluates ONE transcendental chain -- ci_probe(x) -- and the CI is
+// ci_join(cache, probe).  float64: probe = p0(x), join = |cache - probe|; the
+// updated VN n* itself needs two probes, p0(total) (its new cache) and
+// p0(pre_total), taken on two extra lanes of the same pass (kCiSelfLanes) and
+// joined across them.  float32: the probe is the whole cancellation-free CI of
+// (cache = total, x = pre_total), one extra lane.
+template <typename T> struct CiSplit {
+  static constexpr int kSelfLanes = 2;
+  __device__ static __forceinline__ T probe(T /*cache*/, T x) { return p0(x); }
+  __device__ static __forceinline__ T join(T cache, T probe) { return Num<T>::abs_(cache - probe); }
+};
+template <> struct CiSplit<float> {
+  static constexpr int kSelfLanes = 1;
+  __device__ static __forceinline__ float probe(float cache, float x) { return ci_cached<float>(cache, x); }
+  __device__ static __forceinline__ float join(float /*cache*/, float probe) { return probe; }
+};
 
 // ---- exact check-node algebra: input of a V2C, product, product -> C2V.
 //
@@ -324,6 +345,9 @@ struct Grp {
   }
   template <typename V> __device__ __forceinline__ V shfl_up(V v, int d) const {
     return __shfl_up_sync(mask, v, d, G);
+  }
+  template <typename V> __device__ __forceinline__ V shfl_down(V v, int d) const {
+    return __shfl_down_sync(mask, v, d, G);
   }
   __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask, p) >> base; }
   __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }

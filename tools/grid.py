@@ -72,7 +72,7 @@ def main():
             # warm-up on a bounded slice (kernel load, device graph, workspace);
             # the timed decode's outputs are allocated first, outside the events
             o = decode_batch(spec, llr[:min(B, 8192)], cfg)
-            o = {k: torch.zeros((B,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device) for k, v in o.items()}
+            o = {k: torch.zeros((B,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device) for k, v in o.items() if torch.is_tensor(v)}
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
