@@ -29,8 +29,7 @@
 //  * global argmax: 32-ary max trees of order-preserving integer keys, one
 //    coalesced load + REDUX.MAX per level, lowest index wins ties like the
 //    reference's left-preferring segment tree (E:220-257); only the touched
-//    32-leaf groups and their ancestors are recomputed.  Small CI vectors are
-//    scanned flat instead.
+//    32-leaf groups and their ancestors are recomputed.
 #pragma once
 #include "ldpc_common.cuh"
 
@@ -47,7 +46,10 @@ constexpr int dyn_min_blocks(int kind, bool f64) {
   return (f64 && (kind == KIND_RBP || kind == KIND_LMDRBP)) ? 6 : LDPC_DYN_MIN_BLOCKS;
 }
 
-constexpr int kFlatCiMax = 128;  // CIRBP: flat CI argmax when N <= this (else incremental tree)
+
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
 
 // max-tree storage (see "max trees" below)
 template <typename Key>
@@ -90,11 +92,10 @@ struct DynParams {
   unsigned char* ws;      // HBM slots
   long long slotE_bytes, slotN_bytes, slotT_bytes;
   long long o_c2v, o_pre, o_in, o_res;                           // E part
-  long long o_total, o_pretot, o_ci, o_p0t, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
+  long long o_total, o_pretot /* (pre_total, p0t) pairs */, o_ci, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
   long long o_rl1, o_cl1;                                        // T part: level-1 tree nodes
   long long slotU_bytes, o_rup, o_cup;                           // U part (shared memory): tree levels >= 2
   TreeGeom rgeo, cgeo;
-  int flat_ci;            // CIRBP: flat CI argmax instead of a tree
   int scratch_bytes;      // per-warp shared scratch
   int so_items, so_stage, so_nk, so_opre, so_cj, so_ck, so_dl0, so_dl1, so_sizes, so_hist;
   int dl_cap;             // entries of dl0 (twice that allocated: ping-pong for the levels >= 3 fix)
@@ -112,7 +113,12 @@ template <typename T, int G>
 struct Ctx {
   using Key = typename Num<T>::Key;
   Grp<G> w;            // this frame's lane group
-  T *c2v, *pre, *in, *res, *total, *pretot, *ci, *p0t, *tmp;  // p0t = p0_cache(total), CI kinds
+  T *c2v, *pre, *in, *res, *total, *ci, *tmp;
+  // pre_total and p0t = p0_cache(total) (CI kinds) of a VN share one 16-byte
+  // record: the refresh reads both and rewrites pre_total (one sector, not two)
+  T* pp;
+  __device__ __forceinline__ T& pretot(int n) const { return pp[2 * n]; }
+  __device__ __forceinline__ T& p0t(int n) const { return pp[2 * n + 1]; }
   TreeRef<Key> rt, ct;  // residual tree over E, CI tree over N
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
   uint8_t* gid;   // ME kinds: Alg.-4 group of each VN (maintained)
@@ -617,7 +623,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   const T nv = c.pre[e_star];
   const T tot = c.total[n_star] + (nv - old);  // E:147
   T ptn = T(0);  // pre_total of n* (unchanged by this update: the items exclude n*'s edges)
-  if (CI) ptn = c.pretot[n_star];
+  if (CI) ptn = c.pretot(n_star);
   const T cf = act ? c.c2v[adj.x] : T(0);
   if (pf) {
     // stage the two-hop inputs now: they do not depend on this update's V2C
@@ -658,7 +664,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     if (CI)
       for (int n = lane; n < g.N; n += G) {
         p.dump_buf[n] = (double)c.ci[n];
-        p.dump_buf[g.N + n] = (double)c.pretot[n];
+        p.dump_buf[g.N + n] = (double)c.pretot(n);
       }
     for (int e = lane; e < g.E; e += G) {
       p.dump_buf[2 * g.N + 8192 + e] = (double)c.pre[e];
@@ -762,10 +768,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       T cache = T(0), x = T(0);
       if (!dup) {
         if (valid) {
-          x = c.pretot[j] + delta;  // E:171
-          c.pretot[j] = x;
+          const typename Vec2<T>::type pq = *reinterpret_cast<const typename Vec2<T>::type*>(c.pp + 2 * j);
+          x = pq.x + delta;  // E:171
+          c.pretot(j) = x;
           if (CI) {
-            cache = c.p0t[j];  // E:173 (p0(total[j]) cached)
+            cache = pq.y;  // E:173 (p0(total[j]) cached)
             want = true;
             if (CT) c.cj[t] = j;
           }
@@ -776,13 +783,13 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         const int rank = __popc(peers & w.lt);
         const int maxrank = (int)w.rmax(valid ? (unsigned)rank : 0u);
         for (int r = 0; r <= maxrank; ++r) {
-          if (valid && rank == r) c.pretot[j] += delta;
+          if (valid && rank == r) c.pretot(j) += delta;
           w.sync();
         }
         const bool last = valid && ((peers >> lane) >> 1) == 0;
         if (CI && last) {
-          x = c.pretot[j];
-          cache = c.p0t[j];
+          x = c.pretot(j);
+          cache = c.p0t(j);
           want = true;
         }
         if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
@@ -803,7 +810,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
         } else if (self && t == ps0) {
           const T cv = kSelf == 2 ? Num<T>::abs_(pr - pr_next) : pr;
-          c.p0t[n_star] = kSelf == 2 ? pr : tot;  // p0_cache(total[n*])
+          c.p0t(n_star) = kSelf == 2 ? pr : tot;  // p0_cache(total[n*])
           c.ci[n_star] = cv;
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
         }
@@ -942,7 +949,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         // the group's argmax leaf decreased and nothing rose above the old max -> recompute
         const bool dec = valid && ((e == Ic && kk < Qc) || p.dbg_full_tree);
         int bi;
-        const Key km = warp_max_key_minidx_masked(kk, e, peers << w.base, &bi);
+        const Key km = warp_max_key_minidx_masked(kk, e, peers << w.base(), &bi);
         const bool recq = (w.ballot(dec) & peers) != 0 && !(km > Qc);
         bool lrec = false, raisedq = false, holdq = false;
         if (leader) {
@@ -1043,9 +1050,9 @@ __device__ __forceinline__ void fill_remaining(const DynParams& p, long long f, 
 }
 
 template <typename T, int G>
-__device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, const T* pretot, long long f, int k,
+__device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, const T* pp, long long f, int k,
                                            bool conv, const Grp<G>& w) {
-  trace_boundary_rows<T, G>(p.tr, p.g.N, p.i_max, total, pretot, f, k, conv, w);
+  trace_boundary_rows<T, G, 2>(p.tr, p.g.N, p.i_max, total, pp, f, k, conv, w);  // pre_total = pp[2n]
 }
 
 // single-edge boundary rule (E:377-384): returns true when decoding stops
@@ -1058,10 +1065,10 @@ __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c
   if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
     *conv = true;
     fill_remaining<G>(p, f, k, c.w);
-    if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, k, true, c.w);
+    if (TR) trace_rows<T, G>(p, c.total, c.pp, f, k, true, c.w);
     return true;
   }
-  if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, k, false, c.w);
+  if (TR) trace_rows<T, G>(p, c.total, c.pp, f, k, false, c.w);
   return false;
 }
 
@@ -1075,7 +1082,7 @@ __device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int
       *conv = true;
       fill_remaining<G>(p, f, *boundary, c.w);
     }
-    if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, *boundary, *conv, c.w);
+    if (TR) trace_rows<T, G>(p, c.total, c.pp, f, *boundary, *conv, c.w);
     ++(*boundary);
     if (*conv) break;
   }
@@ -1462,8 +1469,8 @@ __device__ Ctx<T, 16> half_ctx(const DynParams& p, const Ctx<T, 32>& c, int half
   Ctx<T, 16> h;
   h.w = Grp<16>::make();
   h.lane = h.w.lane;
-  h.c2v = c.c2v; h.pre = c.pre; h.in = c.in; h.res = c.res; h.total = c.total; h.pretot = c.pretot;
-  h.ci = c.ci; h.p0t = c.p0t; h.tmp = c.tmp;
+  h.c2v = c.c2v; h.pre = c.pre; h.in = c.in; h.res = c.res; h.total = c.total; h.pp = c.pp;
+  h.ci = c.ci; h.tmp = c.tmp;
   h.rt = c.rt; h.ct = c.ct;
   h.inpp = c.inpp; h.gid = c.gid; h.hist = c.hist; h.gbits = c.gbits;
   h.members = c.members; h.sel = c.sel; h.chosen = c.chosen; h.sizes = c.sizes;
@@ -1533,10 +1540,10 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
     for (int n = lane; n < g.N; n += G) {
       T acc = chl(n);
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
-      c.pretot[n] = acc;  // E:121-125
+      c.pretot(n) = acc;  // E:121-125
       if (CI) {
         const T pt = p0_cache(c.total[n]);
-        c.p0t[n] = pt;
+        c.p0t(n) = pt;
         c.ci[n] = ci_cached(pt, acc);
       }
     }
@@ -1616,7 +1623,7 @@ __device__ void me_topm_registers(const DynParams& p, Ctx<T, G>& c, int m, LeafF
   c.w.sync();
 }
 
-template <typename T, int KERNEL, int KF, int G, bool TR, int MODE = 3>
+template <typename T, int KERNEL, int KF, int G, bool TR, int MODE = 3, bool MP = false>
 __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   constexpr bool PF = MODE == 3;
   const int kind = KF >= 0 ? KF : p.kind;  // KF: kind fixed at compile time (-1: runtime)
@@ -1643,7 +1650,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   if (ci_kind) init_state<T, KERNEL, true, G, TR>(p, c, f, kind);
   else init_state<T, KERNEL, false, G, TR>(p, c, f, kind);
   record_boundary<T, G>(p, c.total, f, 0, c.w);
-  if (TR) trace_rows<T, G>(p, c.total, c.pretot, f, 0, false, c.w);
+  if (TR) trace_rows<T, G>(p, c.total, c.pp, f, 0, false, c.w);
   auto rleaf = [&](int e) -> Key { return res_key<T, false, G>(c, e); };
   auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
 
@@ -1660,13 +1667,12 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     } break;
     case KIND_CIRBP: {  // E:388-433
       tree_build(c.rt, p.rgeo, c.w, rleaf);
-      const bool flat = p.flat_ci != 0;
-      if (!flat) tree_build(c.ct, p.cgeo, c.w, cleaf);
+      tree_build(c.ct, p.cgeo, c.w, cleaf);
       const T gamma = (T)p.gamma;
       int kh = 0, kt = 0;  // per-iteration kappa tallies (warp-uniform)
       while (c.prop < budget) {
         const int it = c.it;
-        int n_star = flat ? argmax_scan<Key>(g.N, c.w, cleaf) : tree_argmax(c.ct, p.cgeo, c.w, cleaf);
+        int n_star = tree_argmax(c.ct, p.cgeo, c.w, cleaf);
         c.count(C_CMP, g.N - 1 + 1);
         c.count(C_KTRIALS, 1);
         ++kt;
@@ -1681,8 +1687,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
           c.count(C_CMP, dv_ - 1);
         }
-        if (flat) propagate<T, KERNEL, true, true, false, false, G, false, TR, PF>(p, c, e);
-        else propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
+        propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
         ++c.prop;
         if (c.prop == c.next_b || c.prop >= budget) {
           if (lane == 0) {
@@ -1737,7 +1742,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         int count = select_vns<T, G>(p, c, nullptr, p.n_p, c.sel);
         c.count(C_MSEL, p.n_g);
         for (int idx = 0; idx < count;) {
-          if constexpr (G == 32) {
+          if constexpr (G == 32 && MP) {  // MP: the round-pairing build (opt-in variant)
             if (p.me_pairs && idx + 1 < count && me_pair_disjoint<T>(g, c, c.sel[idx], c.sel[idx + 1], p.pair_cap)) {
               me_pair_step<T, KERNEL, TR, PF>(p, c, idx, nullptr);
               idx += 2;
@@ -1760,7 +1765,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       c.count(C_MSEL, p.n_g);
       while (boundary <= I && !conv) {
         for (int idx = 0; idx < count;) {
-          if constexpr (G == 32) {
+          if constexpr (G == 32 && MP) {  // MP: the round-pairing build (opt-in variant)
             if (p.me_pairs && idx + 1 < count && me_pair_disjoint<T>(g, c, c.sel[idx], c.sel[idx + 1], p.pair_cap)) {
               me_pair_step<T, KERNEL, TR, PF>(p, c, idx, c.chosen);
               idx += 2;
@@ -1869,7 +1874,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
 // MODE 0: E, N and T parts in shared memory; 1: E in HBM, N and T in shared;
 // 2: E and N in HBM, T in shared; 3: everything in HBM.  G lanes per frame
 // (32/G frames per warp); slots and scratch are per frame.
-template <typename T, int KERNEL, int MODE, int KF, int G, bool TR = false>
+template <typename T, int KERNEL, int MODE, int KF, int G, bool TR = false, bool MP = false>
 __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int FPW = 32 / G;  // frames per warp
@@ -1896,9 +1901,8 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   c.in = (T*)(bE + p.o_in);
   c.res = (T*)(bE + p.o_res);
   c.total = (T*)(bN + p.o_total);
-  c.pretot = (T*)(bN + p.o_pretot);
+  c.pp = (T*)(bN + p.o_pretot);
   c.ci = (T*)(bN + p.o_ci);
-  c.p0t = (T*)(bN + p.o_p0t);
   c.tmp = (T*)(bN + p.o_tmp);
   c.inpp = (uint8_t*)(bN + p.o_inpp);
   c.members = (int*)(bN + p.o_members);
@@ -1927,7 +1931,7 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
     if (c.lane == 0) f = atomicAdd(p.next, 1ull);
     f = c.w.shfl(f, 0);
     if ((long long)f >= p.B) break;
-    decode_frame<T, KERNEL, KF, G, TR, MODE>(p, c, (long long)f);
+    decode_frame<T, KERNEL, KF, G, TR, MODE, MP>(p, c, (long long)f);
   }
 }
 
@@ -1962,9 +1966,8 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   c.in = (T*)(bE + p.o_in);
   c.res = (T*)(bE + p.o_res);
   c.total = (T*)(bN + p.o_total);
-  c.pretot = (T*)(bN + p.o_pretot);
+  c.pp = (T*)(bN + p.o_pretot);
   c.ci = (T*)(bN + p.o_ci);
-  c.p0t = (T*)(bN + p.o_p0t);
   c.tmp = (T*)(bN + p.o_tmp);
   c.inpp = (uint8_t*)(bN + p.o_inpp);
   c.members = (int*)(bN + p.o_members);
@@ -2010,7 +2013,7 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   }
   for (int n = c.lane; n < g.N; n += 32) {
     o[2 * g.E + n] = (double)c.total[n];
-    o[2 * g.E + g.N + n] = (double)c.pretot[n];
+    o[2 * g.E + g.N + n] = (double)c.pretot(n);
     o[2 * g.E + 2 * g.N + n] = (double)c.ci[n];
   }
   if (c.lane < kCounters) p.counters[f * kCounters + c.lane] = c.cnt;

@@ -1,0 +1,17 @@
+// Dynamic-schedule kernels: double state, KERNEL_EXACT, multi-edge kinds built
+// with round pairing (LDPC_VARIANT_ME_PAIRS: disjoint consecutive VNs of a round
+// on the two half-warps; exact, measured slower -- kept out of the default kernels).
+#include "dyn_engine.cuh"
+#include "kernel_table.h"
+using namespace ldpc;
+void* dyn_f64_exact_p_get(int mode, int kind) {
+  if (kind == KIND_ME_CIRBP) {
+    switch (mode) {
+      case 0: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 0, KIND_ME_CIRBP, 32, false, true>;
+      case 1: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 1, KIND_ME_CIRBP, 32, false, true>;
+      case 2: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 2, KIND_ME_CIRBP, 32, false, true>;
+      case 3: return (void*)dyn_decode_kernel<double, KERNEL_EXACT, 3, KIND_ME_CIRBP, 32, false, true>;
+    }
+  }
+  return nullptr;
+}

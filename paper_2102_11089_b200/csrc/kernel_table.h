@@ -6,6 +6,8 @@ void* dyn_f64_exact_b_get(int mode, int kind, int g16);
 void* dyn_f64_exact_c_get(int mode, int kind, int g16);
 void* dyn_f64_exact_d_get(int mode, int kind, int g16);
 void* dyn_f64_exact_e_get(int mode, int kind, int g16);
+void* dyn_f64_exact_p_get(int mode, int kind);  // multi-edge kinds built with round pairing
+void* dyn_f64_exact_q_get(int mode, int kind);
 void* dyn_f64_minsum_get(int mode, int kind, int g16);
 void* dyn_f32_exact_get(int mode, int kind, int g16);
 void* dyn_f32_minsum_get(int mode, int kind, int g16);
@@ -17,8 +19,13 @@ void* dyn_trace_f32_minsum_get(int mode);
 // LMDRBP kernel); the other variants dispatch on the kind at run time.
 // g16: 16 lanes per frame (two frames per warp; placement modes 1-3 only).
 // trace: the want_trace build (dyn_trace_*.cu), 32 lanes, kind at run time.
-inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16, int trace = 0) {
+inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16, int trace = 0, int pairs = 0) {
   using namespace ldpc;
+  if (pairs) {  // round-pairing build: float64 exact multi-edge CI kinds, 32 lanes, untraced
+    if (trace || g16 || !f64 || kernel != KERNEL_EXACT) return nullptr;
+    return kind == KIND_ME_CIRBP ? dyn_f64_exact_p_get(mode, kind)
+                                 : kind == KIND_ME_LMD_CIRBP ? dyn_f64_exact_q_get(mode, kind) : nullptr;
+  }
   if (trace) {
     if (g16) return nullptr;
     if (f64) return kernel == KERNEL_EXACT ? dyn_trace_f64_exact_get(mode) : dyn_trace_f64_minsum_get(mode);

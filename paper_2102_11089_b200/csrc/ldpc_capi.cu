@@ -219,10 +219,9 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   // N part
   o = 0;
   p.o_total = take(N * sizeof(T));
-  p.o_pretot = take(ci || s->want_trace ? N * sizeof(T) : 0);
+  p.o_pretot = take(ci || s->want_trace ? 2 * N * sizeof(T) : 0);  // (pre_total, p0(total)) pairs
   p.pt_on = s->want_trace && !ci ? 1 : 0;
   p.o_ci = take(ci ? N * sizeof(T) : 0);
-  p.o_p0t = take(ci ? N * sizeof(T) : 0);
   p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? (N + 3) / 4 * 4 : 0);
   p.fast_sel = (me && s->kind != KIND_ME_RBP && s->n_g <= 255) ? 1 : 0;
   p.o_gid = take(p.fast_sel ? (N + 3) / 4 * 4 : 0);
@@ -236,9 +235,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   o = 0;
   p.rgeo = make_tree((int)E);
   p.cgeo = make_tree((int)N);
-  p.flat_ci = N <= kFlatCiMax ? 1 : 0;
   const bool rt = s->kind == KIND_RBP || s->kind == KIND_CIRBP || s->kind == KIND_ME_RBP;
-  const bool ct = s->kind == KIND_CIRBP && !p.flat_ci;
+  const bool ct = s->kind == KIND_CIRBP;
   p.o_rl1 = take(rt ? p.rgeo.size[1] * (long long)sizeof(L1Node<Key>) : 0);
   p.o_cl1 = take(ct ? p.cgeo.size[1] * (long long)sizeof(L1Node<Key>) : 0);
   p.slotT_bytes = align16(o);
@@ -268,7 +266,9 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.so_hist = (int)stake(p.fast_sel ? s->n_g * 4 : 0);
   // multi-edge round pairing (dyn_engine.cuh me_pair_step): a second copy of
   // the per-update scratch [so_items, so_sizes) for the second half-warp
-  p.me_pairs = (s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && G->d.vn2 &&
+  // (the pairing build exists for float64 exact, untraced; elsewhere the flag is ignored)
+  p.me_pairs = (s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && G->d.vn2 && sizeof(T) == 8 &&
+               s->kernel == KERNEL_EXACT && !s->want_trace && !(s->variant & LDPC_VARIANT_LANES16) &&
                (s->variant & LDPC_VARIANT_ME_PAIRS) ? 1 : 0;
   p.pair_cap = (int)((p.so_nk - p.so_stage) / 4);
   p.so_pair = (int)stake(p.me_pairs ? (long long)(p.so_sizes - p.so_items) : 0);
@@ -276,8 +276,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
 }
 
 template <typename T>
-void* pick_dyn_kernel(int kernel, int mode, int kind, int g16, int trace) {
-  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind, g16, trace);
+void* pick_dyn_kernel(int kernel, int mode, int kind, int g16, int trace, int pairs) {
+  return ldpc_dyn_kernel(sizeof(T) == 8, kernel, mode, kind, g16, trace, pairs);
 }
 
 template <typename T>
@@ -309,7 +309,7 @@ int dyn_plan(const ldpc_graph* G, const ldpc_sched_t* s, long long B, DynPlan& p
     const int fpw = g16 ? 2 : 1;
     const long long per = sh[mode] * fpw;  // shared bytes per warp
     if (per > optin) return c;
-    void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16, s->want_trace);
+    void* fn = pick_dyn_kernel<T>(s->kernel, mode, s->kind, g16, s->want_trace, p.me_pairs);
     if (!fn) return c;
     // warps per block: the size (<= 8) that leaves the most frames resident
     // (shared memory per SM is allocated in whole blocks)
@@ -716,7 +716,7 @@ int decode_impl(const ldpc_graph* G, const void* llr, long long B, const ldpc_sc
     p.ws = (unsigned char*)ws + 256;
     p.tr = tr;
     if (int rc = cuda_check(cudaMemsetAsync(next, 0, 16, st))) return rc;
-    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16, s->want_trace);
+    void* fn = pick_dyn_kernel<T>(s->kernel, pl.mode, s->kind, pl.g16, s->want_trace, pl.p.me_pairs);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_bytes);
     void* args[] = {&p};
     if (int rc = cuda_check(cudaLaunchKernel(fn, dim3(pl.blocks), dim3(pl.warps_per_block * 32), args,

@@ -326,39 +326,43 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 template <int G>
 struct Grp {
   static constexpr int kG = G;
-  unsigned mask;  // warp-level mask of this group's lanes
-  int base;       // first warp lane of the group
-  int lane;       // lane within the group
-  unsigned lt;    // group-local mask of lower lanes
+  unsigned mask_;  // warp-level mask of this group's lanes
+  int base_;       // first warp lane of the group
+  int lane;        // lane within the group
+  unsigned lt;     // group-local mask of lower lanes
+  // a whole warp (G = 32): compile-time constants, so shuffles / votes / syncs
+  // take the immediate full-mask forms
+  __device__ __forceinline__ unsigned mask() const { return G == 32 ? kFull : mask_; }
+  __device__ __forceinline__ int base() const { return G == 32 ? 0 : base_; }
   __device__ __forceinline__ static Grp make() {
     Grp g;
     const int wl = threadIdx.x & 31;
-    g.base = G == 32 ? 0 : (wl / G) * G;
-    g.lane = wl - g.base;
-    g.mask = G == 32 ? kFull : (((1u << G) - 1u) << g.base);
+    g.base_ = G == 32 ? 0 : (wl / G) * G;
+    g.lane = wl - g.base_;
+    g.mask_ = G == 32 ? kFull : (((1u << G) - 1u) << g.base_);
     g.lt = (1u << g.lane) - 1u;
     return g;
   }
-  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask()); }
   template <typename V> __device__ __forceinline__ V shfl(V v, int src) const {
-    return __shfl_sync(mask, v, base + src);
+    return __shfl_sync(mask(), v, base() + src);
   }
   template <typename V> __device__ __forceinline__ V shfl_up(V v, int d) const {
-    return __shfl_up_sync(mask, v, d, G);
+    return __shfl_up_sync(mask(), v, d, G);
   }
   template <typename V> __device__ __forceinline__ V shfl_down(V v, int d) const {
-    return __shfl_down_sync(mask, v, d, G);
+    return __shfl_down_sync(mask(), v, d, G);
   }
-  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask, p) >> base; }
-  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
-  __device__ __forceinline__ unsigned match_any(int v) const { return __match_any_sync(mask, v) >> base; }
-  __device__ __forceinline__ unsigned rmax(unsigned v) const { return __reduce_max_sync(mask, v); }
-  __device__ __forceinline__ unsigned rmin(unsigned v) const { return __reduce_min_sync(mask, v); }
-  __device__ __forceinline__ int rsum(int v) const { return (int)__reduce_add_sync(mask, (unsigned)v); }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask(), p) >> base(); }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask(), p); }
+  __device__ __forceinline__ unsigned match_any(int v) const { return __match_any_sync(mask(), v) >> base(); }
+  __device__ __forceinline__ unsigned rmax(unsigned v) const { return __reduce_max_sync(mask(), v); }
+  __device__ __forceinline__ unsigned rmin(unsigned v) const { return __reduce_min_sync(mask(), v); }
+  __device__ __forceinline__ int rsum(int v) const { return (int)__reduce_add_sync(mask(), (unsigned)v); }
   __device__ __forceinline__ int incl_scan(int v) const {
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-      int t = __shfl_up_sync(mask, v, d, G);
+      int t = __shfl_up_sync(mask(), v, d, G);
       if (lane >= d) v += t;
     }
     return v;
@@ -401,7 +405,7 @@ struct Grp {
 // Rows of boundary k (E:204-207) -- and, once converged, of every later
 // boundary (E:215-217) -- plus their J(gamma) counts, D = |p0(total) -
 // p0(pre_total)| in float64 like the reference's post-processing of the trace.
-template <typename T, int G>
+template <typename T, int G, int PS = 1>  // PS: stride of the pre_total column
 __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* total, const T* pretot, long long f,
                                     int k, bool conv, const Grp<G>& w) {
   if (!to.trace && !to.jc) return;
@@ -411,7 +415,7 @@ __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* t
       double* row = to.trace + (f * (I + 1) + kk) * 2ll * N;
       for (int n = w.lane; n < N; n += G) {
         row[n] = (double)total[n];
-        row[N + n] = (double)pretot[n];
+        row[N + n] = (double)pretot[PS * n];
       }
     }
   if (to.jc)
@@ -420,7 +424,7 @@ __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* t
       int ok = 0, bad = 0;
       for (int n = w.lane; n < N; n += G) {
         const double t = (double)total[n];
-        const double d = fabs(p0(t) - p0((double)pretot[n]));
+        const double d = fabs(p0(t) - p0((double)pretot[PS * n]));
         if (d >= gm) {
           if (t >= 0.0) ++ok;
           else ++bad;
