@@ -42,14 +42,40 @@ namespace ldpc {
 // registers) in general; the float64 RBP and LMDRBP kernels run faster at 6
 // (40 registers, more spills, 1.5x the resident frames: C1 -3 % / -16 %),
 // while the CI and ME kinds lose (measured with tools/dyn_sweep.py).
-constexpr int dyn_min_blocks(int kind, bool f64) {
-  return (f64 && (kind == KIND_RBP || kind == KIND_LMDRBP)) ? 6 : LDPC_DYN_MIN_BLOCKS;
+#ifndef LDPC_DYN_RBP_BLOCKS
+#define LDPC_DYN_RBP_BLOCKS 6
+#endif
+// BG-sized codes (placement mode 3: the whole state in HBM) are bound by the
+// memory system's sector-request rate, where spill traffic competes with the
+// state traffic and shared memory already caps the resident warps: RBP runs
+// faster at 4 blocks (64 registers; C3 2.39e8 vs 1.76e8 updates/s) and CIRBP at
+// 3 (80 registers; C3 6.2e7 vs 5.1e7).
+constexpr int dyn_min_blocks(int kind, bool f64, int mode) {
+  if (f64 && mode == 3 && (kind == KIND_RBP || kind == KIND_LMDRBP)) return 4;
+  if (f64 && mode == 3 && kind == KIND_CIRBP) return 3;
+  return (f64 && (kind == KIND_RBP || kind == KIND_LMDRBP)) ? LDPC_DYN_RBP_BLOCKS : LDPC_DYN_MIN_BLOCKS;
 }
 
 
 template <typename T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
+
+// Two-hop item record (8 bytes: the table of a BG1-sized code is read from HBM
+// on every update, so its size is DRAM traffic): edge g, and packed the
+// position of g in its check (skip), the check's degree d and the base of the
+// check's inputs in the stage area.
+struct Item { int g, skip, d, sb; };
+__host__ __device__ __forceinline__ int pack_item(int skip, int d, int sb) { return skip | (d << 8) | (sb << 16); }
+__device__ __forceinline__ Item unpack_item(int2 r) {
+  Item it;
+  it.g = r.x;
+  it.skip = r.y & 0xff;
+  it.d = (r.y >> 8) & 0xff;
+  it.sb = (int)((unsigned)r.y >> 16);
+  return it;
+}
+constexpr int kItemMaxDegree = 255, kItemMaxStage = 65535;
 
 // max-tree storage (see "max trees" below)
 template <typename Key>
@@ -92,7 +118,7 @@ struct DynParams {
   unsigned char* ws;      // HBM slots
   long long slotE_bytes, slotN_bytes, slotT_bytes;
   long long o_c2v, o_pre, o_in, o_res;                           // E part
-  long long o_total, o_pretot /* (pre_total, p0t) pairs */, o_ci, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
+  long long o_total /* per-VN records or dense totals */, o_inpp, o_gid, o_gbits, o_members, o_sel, o_chosen, o_tmp;  // N part
   long long o_rl1, o_cl1;                                        // T part: level-1 tree nodes
   long long slotU_bytes, o_rup, o_cup;                           // U part (shared memory): tree levels >= 2
   TreeGeom rgeo, cgeo;
@@ -113,20 +139,28 @@ template <typename T, int G>
 struct Ctx {
   using Key = typename Num<T>::Key;
   Grp<G> w;            // this frame's lane group
-  T *c2v, *pre, *in, *res, *total, *ci, *tmp;
-  // pre_total and p0t = p0_cache(total) (CI kinds) of a VN share one 16-byte
-  // record: the refresh reads both and rewrites pre_total (one sector, not two)
-  T* pp;
-  __device__ __forceinline__ T& pretot(int n) const { return pp[2 * n]; }
-  __device__ __forceinline__ T& p0t(int n) const { return pp[2 * n + 1]; }
+  T *c2v, *pre, *in, *res, *tmp;
+  // Per-VN state: one record per VN, (pre_total, p0t = p0_cache(total), total,
+  // ci) -- 4 words, one 32-byte sector in float64 -- because a CI-kind update
+  // touches these words of ~90 scattered VNs and HBM moves whole sectors: one
+  // sector per VN instead of three.  (The RBP family uses only `total`; the
+  // record keeps one base pointer and immediate offsets for every kind.)
+  T* nb;   // records
+  int cs;  // stride of ci in words: 4 (records); 1 when nb = a caller's dense CI vector - 3 (ldpc_select_vns)
+  static constexpr int ts = 4;  // stride of total in words
+  __device__ __forceinline__ T* tb() const { return nb + 2; }
+  __device__ __forceinline__ T& total(int n) const { return nb[4 * n + 2]; }
+  __device__ __forceinline__ T& pretot(int n) const { return nb[4 * n]; }
+  __device__ __forceinline__ T& p0t(int n) const { return nb[4 * n + 1]; }
+  __device__ __forceinline__ T& ci(int n) const { return nb[cs * n + 3]; }
   TreeRef<Key> rt, ct;  // residual tree over E, CI tree over N
   uint8_t* inpp;  // ME-LMD-CIRBP P' membership (E:665)
   uint8_t* gid;   // ME kinds: Alg.-4 group of each VN (maintained)
   int* hist;      // ME kinds: VNs per group (maintained)
   unsigned* gbits;  // ME kinds: membership bitmap of each group (maintained)
   int *members, *sel, *chosen;
-  const int4* items;  // two-hop edges of the last update (g, a, d, stage base), ascending g
-  int4* items_buf;    // per-warp scratch for items built on the fly
+  const int2* items;  // two-hop edges of the last update, ascending g: (g, packed skip | d | stage base)
+  int2* items_buf;    // per-warp scratch for items built on the fly
   T* stage;       // staged check inputs of the last update
   Key* nk;        // new residual key of each item
   T* cg;          // C2V of each item, staged with its inputs (aliases nk: read before nk is written)
@@ -135,7 +169,13 @@ struct Ctx {
   Key* ck;        // CI key of each item's VN after the refresh (CI tree; aliases opre, read first)
   int *dl0, *dl1; // dirty-node lists for tree maintenance
   int* sizes;     // Alg.4 group histogram
-  long long cnt;     // work counters (E:17-25), one per lane: lane k holds counter k
+  // work counters (E:17-25): the 8 words just below the stage area of the
+  // frame's shared scratch (addressed off `stage`: no register of their own)
+  long long* cbase;  // half-warp contexts of a pair step (G = 16): the frame's counters; unused for G = 32
+  __device__ __forceinline__ long long* cntp() const {
+    if constexpr (G == 32) return (long long*)stage - kCounters;
+    else return cbase;
+  }
   long long prop;
   long long cur_f;   // frame being decoded
   int nsel;          // Alg.-4 selections made (debug log index)
@@ -144,7 +184,10 @@ struct Ctx {
   int lane;          // lane within the group (= w.lane)
   long long rng;
   __device__ __forceinline__ void count(int k, long long v) {
-    if (lane == k) cnt += v;
+    if (lane == 0) {
+      if (G == 32) cntp()[k] += v;
+      else atomicAdd((unsigned long long*)&cntp()[k], (unsigned long long)v);  // half-warps of a pair step share them
+    }
   }
 };
 
@@ -530,7 +573,7 @@ __device__ __forceinline__ int build_items_from(Ctx<T, G>& c, int4 adj, bool act
   if (act) {
     int t = t0;
     for (int e = adj.z; e < adj.w; ++e)
-      if (e != adj.x) c.items_buf[t++] = make_int4(e, adj.z, d, sbase);
+      if (e != adj.x) c.items_buf[t++] = make_int2(e, pack_item(e - adj.z, d, sbase));
   }
   *sbase_out = sbase;
   carry_items += total & 0xffff;
@@ -569,8 +612,9 @@ __device__ __forceinline__ int ci_group(T v, int n_g) {
 // group-size histogram and one membership bitmap per group (n_g x W words,
 // W = ceil(N/32)), so a selection round reads k*+1 bitmap rows, not N CIs.
 template <typename T, int G>
-__device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int j, T v) {
-  const int gn = ci_group(v, n_g), go = c.gid[j];
+__device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int j, T v, T v_old) {
+  // the old group follows from the old CI (read with the VN's record) -- no load of gid[j]
+  const int gn = ci_group(v, n_g), go = ci_group(v_old, n_g);
   if (gn != go) {
     atomicSub(&c.hist[go], 1);
     atomicAdd(&c.hist[gn], 1);
@@ -619,11 +663,15 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   int4 adj = make_int4(-1, -1, 0, 0);
   if (lane < vr.y) adj = g.vadj[vr.x + lane];
   const bool act = lane < vr.y && adj.y != m_star;
+  int sb0 = 0;  // stage base of this lane's check (loaded with the records above, not after the commit)
+  if (tab && lane < vr.y) sb0 = g.hop_sb[hsp + lane];
   const T old = c.c2v[e_star];
   const T nv = c.pre[e_star];
-  const T tot = c.total[n_star] + (nv - old);  // E:147
+  const T tot = c.total(n_star) + (nv - old);  // E:147
   T ptn = T(0);  // pre_total of n* (unchanged by this update: the items exclude n*'s edges)
+  T cin = T(0);  // CI of n* before this update (its Alg.-4 group)
   if (CI) ptn = c.pretot(n_star);
+  if (CI && MG) cin = c.ci(n_star);
   const T cf = act ? c.c2v[adj.x] : T(0);
   if (pf) {
     // stage the two-hop inputs now: they do not depend on this update's V2C
@@ -631,27 +679,27 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     // with pre_total upkeep, its old pre) for the refresh; two items per pass
     for (int t = lane; t < n_items; t += 2 * G) {
       const int t2 = t + G;
-      const int4 r = c.items[t];
-      int4 r2 = r;
-      if (t2 < n_items) r2 = c.items[t2];
-      const T x = c.in[r.x], cg = c.c2v[r.x];
-      const T x2 = c.in[r2.x], cg2 = c.c2v[r2.x];
+      const Item r = unpack_item(c.items[t]);
+      Item r2 = r;
+      if (t2 < n_items) r2 = unpack_item(c.items[t2]);
+      const T x = c.in[r.g], cg = c.c2v[r.g];
+      const T x2 = c.in[r2.g], cg2 = c.c2v[r2.g];
       T op = T(0), op2 = T(0);
       int j1 = 0, j2 = 0;
       if (PT) {
-        op = c.pre[r.x];
-        op2 = c.pre[r2.x];
-        j1 = g.edge_vn[r.x];
-        j2 = g.edge_vn[r2.x];
+        op = c.pre[r.g];
+        op2 = c.pre[r2.g];
+        j1 = g.edge_vn[r.g];
+        j2 = g.edge_vn[r2.g];
       }
-      c.stage[r.w + (r.x - r.y)] = x;
+      c.stage[r.sb + r.skip] = x;
       c.cg[t] = cg;
       if (PT) {
         c.opre[t] = op;
         c.cj[t] = j1;
       }
       if (t2 < n_items) {
-        c.stage[r2.w + (r2.x - r2.y)] = x2;
+        c.stage[r2.sb + r2.skip] = x2;
         c.cg[t2] = cg2;
         if (PT) {
           c.opre[t2] = op2;
@@ -663,7 +711,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   if (p.dump_buf && c.cur_f == 0 && c.prop == p.dump_step) {
     if (CI)
       for (int n = lane; n < g.N; n += G) {
-        p.dump_buf[n] = (double)c.ci[n];
+        p.dump_buf[n] = (double)c.ci(n);
         p.dump_buf[g.N + n] = (double)c.pretot(n);
       }
     for (int e = lane; e < g.E; e += G) {
@@ -679,7 +727,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     c.c2v[e_star] = nv;
     if (STORED) c.res[e_star] = T(0);
-    c.total[n_star] = tot;  // n*'s own CI (E:148-149) is evaluated on spare lanes of the refresh below
+    c.total(n_star) = tot;  // n*'s own CI (E:148-149) is evaluated on spare lanes of the refresh below
   }
   // V2C to the other checks of n* (E:153-160), also staged; slots in chunks of G
   int ci_ = 0, cs_ = 0;
@@ -696,7 +744,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     int sbase = 0;
     if (tab) {
-      if (k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
+      sbase = sb0;
+      if (k0 > 0 && k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
     } else {
       n_items = build_items_from<T, G>(c, a2, act2, &sbase, ci_, cs_);
     }
@@ -710,8 +759,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   w.sync();
   if (!pf) {
     for (int t = lane; t < n_items; t += G) {  // stage the rest of each check
-      int4 r = c.items[t];
-      c.stage[r.w + (r.x - r.y)] = c.in[r.x];
+      const Item r = unpack_item(c.items[t]);
+      c.stage[r.sb + r.skip] = c.in[r.g];
     }
     w.sync();
   }
@@ -731,8 +780,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int j = -1;
     T delta = T(0);
     if (valid) {
-      const int4 r = c.items[t];
-      const int ge = r.x, skip = r.x - r.y;
+      const Item r = unpack_item(c.items[t]);
+      const int ge = r.g, skip = r.skip;
       // independent loads first (the pre[] store below would otherwise pin them)
       const T cg = pf ? c.cg[t] : c.c2v[ge];
       T opre = T(0);
@@ -740,22 +789,22 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         j = pf ? c.cj[t] : g.edge_vn[ge];
         opre = pf ? c.opre[t] : c.pre[ge];
       }
-      const T* s = c.stage + r.w;
+      const T* s = c.stage + r.sb;
       T np_;
       if (KERNEL == KERNEL_EXACT) {
         T prod = cn_one<T>();
-        for (int q = 0; q < r.z; ++q)
+        for (int q = 0; q < r.d; ++q)
           if (q != skip) prod = cn_mul(prod, s[q]);
-        np_ = atanh_msg(prod, r.z - 1);
+        np_ = atanh_msg(prod, r.d - 1);
       } else {
         T sign = T(1), mag = Num<T>::kBig;
-        for (int q = 0; q < r.z; ++q) {
+        for (int q = 0; q < r.d; ++q) {
           if (q == skip) continue;
           T v = clampv(s[q]);
           if (v < T(0)) { sign = -sign; v = -v; }
           if (v < mag) mag = v;
         }
-        np_ = r.z > 1 ? clampv(sign * mag) : T(0);
+        np_ = r.d > 1 ? clampv(sign * mag) : T(0);
       }
       if (PT) delta = np_ - opre;
       c.pre[ge] = np_;
@@ -765,10 +814,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     if (PT) {
       bool want = false;  // this lane evaluates a CI: (cache, x) -> probe
-      T cache = T(0), x = T(0);
+      T cache = T(0), x = T(0), oci = T(0);
       if (!dup) {
         if (valid) {
-          const typename Vec2<T>::type pq = *reinterpret_cast<const typename Vec2<T>::type*>(c.pp + 2 * j);
+          const typename Vec2<T>::type pq = *reinterpret_cast<const typename Vec2<T>::type*>(c.nb + 4 * j);
+          if (CI && MG) oci = c.ci(j);  // same sector as pq
           x = pq.x + delta;  // E:171
           c.pretot(j) = x;
           if (CI) {
@@ -790,6 +840,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (CI && last) {
           x = c.pretot(j);
           cache = c.p0t(j);
+          if (MG) oci = c.ci(j);
           want = true;
         }
         if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
@@ -805,14 +856,14 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (kSelf == 2) pr_next = w.shfl_down(pr, 1);
         if (want) {
           const T cv = CiSplit<T>::join(cache, pr);
-          c.ci[j] = cv;
+          c.ci(j) = cv;
           if (CT) c.ck[t] = Num<T>::key(cv);
-          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv);
+          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv, oci);
         } else if (self && t == ps0) {
           const T cv = kSelf == 2 ? Num<T>::abs_(pr - pr_next) : pr;
           c.p0t(n_star) = kSelf == 2 ? pr : tot;  // p0_cache(total[n*])
-          c.ci[n_star] = cv;
-          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv);
+          c.ci(n_star) = cv;
+          if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, n_star, cv, cin);
         }
       }
     }
@@ -984,7 +1035,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int* se = (int*)c.stage;  // stage is free again: G (index, key) pairs
     Key* sk = (Key*)(se + 32);
     int nrec = 0, ndirty = 0;
-    apply_leaf_updates(c.ct, geo, lane == 0 ? n_star : -1, Num<T>::key(c.ci[n_star]), w, se, sk, c.dl1, nrec,
+    apply_leaf_updates(c.ct, geo, lane == 0 ? n_star : -1, Num<T>::key(c.ci(n_star)), w, se, sk, c.dl1, nrec,
                        c.dl0, ndirty);
     for (int base = 0; base < n_items; base += G) {  // (VN, key) pairs staged by the refresh
       const int t = base + lane;
@@ -996,7 +1047,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       }
       apply_leaf_updates(c.ct, geo, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
     }
-    auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
+    auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci(n)); };
     group_recompute_list(c.ct, geo, c.dl1, nrec, w, cleaf);
     w.sync();
     l2_finish(c.ct, geo, c.dl1, nrec, c.dl0, ndirty, c.dl0 + (geo.levels > 2 ? p.dl_cap : 0), w, cleaf);
@@ -1012,22 +1063,22 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
 // ------------------------------------------------------------ boundaries
 
 template <typename T, int G>
-__device__ bool syndrome_ok(const DevGraph& g, const T* total, const Grp<G>& w) {  // E:179-188
+__device__ bool syndrome_ok(const DevGraph& g, const T* total, int ts, const Grp<G>& w) {  // E:179-188
   for (int base = 0; base < g.M; base += G) {
     const int m = base + w.lane;
     int par = 0;
     if (m < g.M)
-      for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e) par ^= (total[g.edge_vn[e]] < T(0)) ? 1 : 0;
+      for (int e = g.cn_ptr[m]; e < g.cn_ptr[m + 1]; ++e) par ^= (total[g.edge_vn[e] * ts] < T(0)) ? 1 : 0;
     if (w.any(par)) return false;
   }
   return true;
 }
 
 template <typename T, int G>
-__device__ void record_boundary(const DynParams& p, const T* total, long long f, int k, const Grp<G>& w) {
+__device__ void record_boundary(const DynParams& p, const T* total, int ts, long long f, int k, const Grp<G>& w) {
   int errs = 0, ei = 0;
   for (int n = w.lane; n < p.g.N; n += G)
-    if (total[n] < T(0)) {
+    if (total[n * ts] < T(0)) {
       ++errs;
       if (n < p.k_info) ++ei;
     }
@@ -1050,9 +1101,9 @@ __device__ __forceinline__ void fill_remaining(const DynParams& p, long long f, 
 }
 
 template <typename T, int G>
-__device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, const T* pp, long long f, int k,
+__device__ __forceinline__ void trace_rows(const DynParams& p, const T* total, const T* nb, long long f, int k,
                                            bool conv, const Grp<G>& w) {
-  trace_boundary_rows<T, G, 2>(p.tr, p.g.N, p.i_max, total, pp, f, k, conv, w);  // pre_total = pp[2n]
+  trace_boundary_rows<T, G, 4>(p.tr, p.g.N, p.i_max, total, nb, f, k, conv, w);  // records: total = nb[4n+2], pre_total = nb[4n]
 }
 
 // single-edge boundary rule (E:377-384): returns true when decoding stops
@@ -1061,14 +1112,14 @@ __device__ __forceinline__ bool single_boundary(const DynParams& p, Ctx<T, G>& c
   if (c.prop != c.next_b) return false;
   c.next_b += p.g.E;
   const int k = ++c.it;
-  record_boundary<T, G>(p, c.total, f, k, c.w);
-  if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
+  record_boundary<T, G>(p, c.tb(), c.ts, f, k, c.w);
+  if (syndrome_ok<T, G>(p.g, c.tb(), c.ts, c.w)) {
     *conv = true;
     fill_remaining<G>(p, f, k, c.w);
-    if (TR) trace_rows<T, G>(p, c.total, c.pp, f, k, true, c.w);
+    if (TR) trace_rows<T, G>(p, c.tb(), c.nb, f, k, true, c.w);
     return true;
   }
-  if (TR) trace_rows<T, G>(p, c.total, c.pp, f, k, false, c.w);
+  if (TR) trace_rows<T, G>(p, c.tb(), c.nb, f, k, false, c.w);
   return false;
 }
 
@@ -1077,12 +1128,12 @@ template <typename T, int G, bool TR>
 __device__ void me_boundaries(const DynParams& p, Ctx<T, G>& c, long long f, int* boundary, bool* conv) {
   const long long E = p.g.E;
   while (*boundary <= p.i_max && c.prop >= (long long)(*boundary) * E) {
-    record_boundary<T, G>(p, c.total, f, *boundary, c.w);
-    if (syndrome_ok<T, G>(p.g, c.total, c.w)) {
+    record_boundary<T, G>(p, c.tb(), c.ts, f, *boundary, c.w);
+    if (syndrome_ok<T, G>(p.g, c.tb(), c.ts, c.w)) {
       *conv = true;
       fill_remaining<G>(p, f, *boundary, c.w);
     }
-    if (TR) trace_rows<T, G>(p, c.total, c.pp, f, *boundary, *conv, c.w);
+    if (TR) trace_rows<T, G>(p, c.tb(), c.nb, f, *boundary, *conv, c.w);
     ++(*boundary);
     if (*conv) break;
   }
@@ -1312,7 +1363,7 @@ __device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl,
   for (int q = lane; q < n_g; q += G) c.sizes[q] = 0;
   c.w.sync();
   for (int n = lane; n < N; n += G)
-    if (!excl || !excl[n]) atomicAdd(&c.sizes[ci_group(c.ci[n], n_g)], 1);
+    if (!excl || !excl[n]) atomicAdd(&c.sizes[ci_group(c.ci(n), n_g)], 1);
   c.w.sync();
   int sel_total;
   const int k_star = kstar_of(c, c.sizes, n_g, n_p, &sel_total);
@@ -1322,7 +1373,7 @@ __device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl,
   for (int base = 0; base < N; base += G) {
     const int n = base + lane;
     int gi = -1;
-    if (n < N && (!excl || !excl[n])) gi = ci_group(c.ci[n], n_g);
+    if (n < N && (!excl || !excl[n])) gi = ci_group(c.ci(n), n_g);
     const bool s = gi >= thr, f = want_fill && gi == fill;
     const unsigned bs = c.w.ballot(s), bf = c.w.ballot(f);
     if (s) out[count + __popc(bs & c.w.lt)] = n;
@@ -1405,7 +1456,7 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
     for (int e = a + lane; e < b; e += G)
       if (e != e_prev) {
         int j = g.edge_vn[e];
-        Key k = Num<T>::key(c.ci[j]);
+        Key k = Num<T>::key(c.ci(j));
         if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
       }
   } else {
@@ -1413,7 +1464,7 @@ __device__ int ci_argmax_twohop(const DynParams& p, Ctx<T, G>& c, int e_prev, in
     ncand = g.hop_distinct[e_prev];
     for (int t = lane; t < n_items; t += G) {
       int j = g.edge_vn[c.items[t].x];
-      Key k = Num<T>::key(c.ci[j]);
+      Key k = Num<T>::key(c.ci(j));
       if (k > bk || (k == bk && j < bj)) { bk = k; bj = j; }
     }
   }
@@ -1469,8 +1520,8 @@ __device__ Ctx<T, 16> half_ctx(const DynParams& p, const Ctx<T, 32>& c, int half
   Ctx<T, 16> h;
   h.w = Grp<16>::make();
   h.lane = h.w.lane;
-  h.c2v = c.c2v; h.pre = c.pre; h.in = c.in; h.res = c.res; h.total = c.total; h.pp = c.pp;
-  h.ci = c.ci; h.tmp = c.tmp;
+  h.c2v = c.c2v; h.pre = c.pre; h.in = c.in; h.res = c.res; h.nb = c.nb; h.cs = c.cs;
+  h.tmp = c.tmp;
   h.rt = c.rt; h.ct = c.ct;
   h.inpp = c.inpp; h.gid = c.gid; h.hist = c.hist; h.gbits = c.gbits;
   h.members = c.members; h.sel = c.sel; h.chosen = c.chosen; h.sizes = c.sizes;
@@ -1486,7 +1537,7 @@ __device__ Ctx<T, 16> half_ctx(const DynParams& p, const Ctx<T, 32>& c, int half
   h.ck = sh(c.ck);
   h.dl0 = sh(c.dl0);
   h.dl1 = sh(c.dl1);
-  h.cnt = 0;
+  h.cbase = c.cntp();  // both halves add (atomically) into the frame's counters
   h.prop = c.prop + half;
   h.cur_f = c.cur_f;
   h.nsel = c.nsel;
@@ -1508,8 +1559,6 @@ __device__ void me_pair_step(const DynParams& p, Ctx<T, 32>& c, int idx, int* ch
   if (chosen && h.lane == 0) chosen[idx + half] = e;
   propagate<T, KERNEL, true, false, false, false, 16, true, TR, PF>(p, h, e);
   __syncwarp();
-  // half lane k holds counter k of its half: full-warp lanes k < 8 collect both
-  c.cnt += h.cnt + __shfl_xor_sync(kFull, h.cnt, 16);
   c.prop += 2;
 }
 
@@ -1529,7 +1578,7 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
     c.c2v[e] = T(0);
     c.in[e] = (KERNEL == KERNEL_EXACT) ? cn_in<T>(v) : v;
   }
-  for (int n = lane; n < g.N; n += G) c.total[n] = chl(n);
+  for (int n = lane; n < g.N; n += G) c.total(n) = chl(n);
   c.w.sync();
   for (int m = lane; m < g.M; m += G) {
     int a = g.cn_ptr[m], b = g.cn_ptr[m + 1];
@@ -1542,9 +1591,9 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
       for (int k = g.vn_ptr[n]; k < g.vn_ptr[n + 1]; ++k) acc += c.pre[g.vn_edges[k]];
       c.pretot(n) = acc;  // E:121-125
       if (CI) {
-        const T pt = p0_cache(c.total[n]);
+        const T pt = p0_cache(c.total(n));
         c.p0t(n) = pt;
-        c.ci[n] = ci_cached(pt, acc);
+        c.ci(n) = ci_cached(pt, acc);
       }
     }
   if ((kind == KIND_ME_CIRBP || kind == KIND_ME_LMD_CIRBP) && p.fast_sel) {
@@ -1553,7 +1602,7 @@ __device__ void init_state(const DynParams& p, Ctx<T, G>& c, long long f, int ki
     for (int q = lane; q < p.n_g * W; q += G) c.gbits[q] = 0u;
     c.w.sync();
     for (int n = lane; n < g.N; n += G) {
-      const int gi = ci_group(c.ci[n], p.n_g);
+      const int gi = ci_group(c.ci(n), p.n_g);
       c.gid[n] = (uint8_t)gi;
       atomicAdd(&c.hist[gi], 1);
       atomicOr(&c.gbits[gi * W + (n >> 5)], 1u << (n & 31));
@@ -1632,7 +1681,8 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   const DevGraph& g = p.g;
   const long long E = g.E, budget = (long long)p.i_max * E;
   const int lane = c.lane, I = p.i_max;
-  c.cnt = 0;
+  if (lane < kCounters) c.cntp()[lane] = 0;
+  c.w.sync();
   c.prop = 0;
   c.cur_f = f;
   c.nsel = 0;
@@ -1649,10 +1699,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
                        kind == KIND_ME_LMD_CIRBP;
   if (ci_kind) init_state<T, KERNEL, true, G, TR>(p, c, f, kind);
   else init_state<T, KERNEL, false, G, TR>(p, c, f, kind);
-  record_boundary<T, G>(p, c.total, f, 0, c.w);
-  if (TR) trace_rows<T, G>(p, c.total, c.pp, f, 0, false, c.w);
+  record_boundary<T, G>(p, c.tb(), c.ts, f, 0, c.w);
+  if (TR) trace_rows<T, G>(p, c.tb(), c.nb, f, 0, false, c.w);
   auto rleaf = [&](int e) -> Key { return res_key<T, false, G>(c, e); };
-  auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci[n]); };
+  auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci(n)); };
 
   switch (kind) {
     case KIND_RBP: {  // E:355-385
@@ -1676,7 +1726,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
         c.count(C_CMP, g.N - 1 + 1);
         c.count(C_KTRIALS, 1);
         ++kt;
-        bool hit = c.ci[n_star] < gamma;
+        bool hit = c.ci(n_star) < gamma;
         int e;
         if (hit) {
           c.count(C_KHITS, 1);
@@ -1861,9 +1911,10 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     default:
       break;
   }
-  if (I == 0) conv = syndrome_ok<T, G>(g, c.total, c.w);  // schedules.py:144-146
-  for (int n = lane; n < g.N; n += G) p.u_hat[f * g.N + n] = c.total[n] < T(0) ? 1 : 0;
-  if (lane < kCounters) p.counters[f * kCounters + lane] = c.cnt;
+  if (I == 0) conv = syndrome_ok<T, G>(g, c.tb(), c.ts, c.w);  // schedules.py:144-146
+  for (int n = lane; n < g.N; n += G) p.u_hat[f * g.N + n] = c.total(n) < T(0) ? 1 : 0;
+  c.w.sync();
+  if (lane < kCounters) p.counters[f * kCounters + lane] = c.cntp()[lane];
   if (lane == 0) {
     p.prop[f] = c.prop;
     p.conv[f] = conv ? 1 : 0;
@@ -1875,7 +1926,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
 // 2: E and N in HBM, T in shared; 3: everything in HBM.  G lanes per frame
 // (32/G frames per warp); slots and scratch are per frame.
 template <typename T, int KERNEL, int MODE, int KF, int G, bool TR = false, bool MP = false>
-__global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_decode_kernel(const __grid_constant__ DynParams p) {
+__global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8, MODE)) dyn_decode_kernel(const __grid_constant__ DynParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int FPW = 32 / G;  // frames per warp
   const int fpb = (blockDim.x >> 5) * FPW;
@@ -1900,9 +1951,8 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   c.pre = (T*)(bE + p.o_pre);
   c.in = (T*)(bE + p.o_in);
   c.res = (T*)(bE + p.o_res);
-  c.total = (T*)(bN + p.o_total);
-  c.pp = (T*)(bN + p.o_pretot);
-  c.ci = (T*)(bN + p.o_ci);
+  c.nb = (T*)(bN + p.o_total);
+  c.cs = 4;
   c.tmp = (T*)(bN + p.o_tmp);
   c.inpp = (uint8_t*)(bN + p.o_inpp);
   c.members = (int*)(bN + p.o_members);
@@ -1912,7 +1962,7 @@ __global__ void __launch_bounds__(256, dyn_min_blocks(KF, sizeof(T) == 8)) dyn_d
   c.rt.up = (Key*)(bU + p.o_rup);
   c.ct.l1 = (L1Node<Key>*)(bT + p.o_cl1);
   c.ct.up = (Key*)(bU + p.o_cup);
-  c.items_buf = (int4*)(scr + p.so_items);
+  c.items_buf = (int2*)(scr + p.so_items);
   c.items = c.items_buf;
   c.stage = (T*)(scr + p.so_stage);
   c.nk = (Key*)(scr + p.so_nk);
@@ -1965,9 +2015,8 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   c.pre = (T*)(bE + p.o_pre);
   c.in = (T*)(bE + p.o_in);
   c.res = (T*)(bE + p.o_res);
-  c.total = (T*)(bN + p.o_total);
-  c.pp = (T*)(bN + p.o_pretot);
-  c.ci = (T*)(bN + p.o_ci);
+  c.nb = (T*)(bN + p.o_total);
+  c.cs = 4;
   c.tmp = (T*)(bN + p.o_tmp);
   c.inpp = (uint8_t*)(bN + p.o_inpp);
   c.members = (int*)(bN + p.o_members);
@@ -1979,7 +2028,7 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   c.rt.up = (Key*)(bU + p.o_rup);
   c.ct.l1 = (L1Node<Key>*)(bT + p.o_cl1);
   c.ct.up = (Key*)(bU + p.o_cup);
-  c.items_buf = (int4*)(scr + p.so_items);
+  c.items_buf = (int2*)(scr + p.so_items);
   c.items = c.items_buf;
   c.stage = (T*)(scr + p.so_stage);
   c.nk = (Key*)(scr + p.so_nk);
@@ -1991,7 +2040,8 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
   c.dl1 = (int*)(scr + p.so_dl1);
   c.sizes = (int*)(scr + p.so_sizes);
   c.hist = (int*)(scr + p.so_hist);
-  c.cnt = 0;
+  if (c.lane < kCounters) c.cntp()[c.lane] = 0;
+  c.w.sync();
   c.prop = 0;
   c.cur_f = f;
   c.nsel = 0;
@@ -2012,11 +2062,12 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
     o[g.E + e] = (double)c.pre[e];
   }
   for (int n = c.lane; n < g.N; n += 32) {
-    o[2 * g.E + n] = (double)c.total[n];
+    o[2 * g.E + n] = (double)c.total(n);
     o[2 * g.E + g.N + n] = (double)c.pretot(n);
-    o[2 * g.E + 2 * g.N + n] = (double)c.ci[n];
+    o[2 * g.E + 2 * g.N + n] = (double)c.ci(n);
   }
-  if (c.lane < kCounters) p.counters[f * kCounters + c.lane] = c.cnt;
+  c.w.sync();
+  if (c.lane < kCounters) p.counters[f * kCounters + c.lane] = c.cntp()[c.lane];
 }
 
 }  // namespace ldpc

@@ -10,6 +10,7 @@ void* dyn_f64_exact_p_get(int mode, int kind);  // multi-edge kinds built with r
 void* dyn_f64_exact_q_get(int mode, int kind);
 void* dyn_f64_minsum_get(int mode, int kind, int g16);
 void* dyn_f32_exact_get(int mode, int kind, int g16);
+void* dyn_f32_exact_k_get(int mode, int kind);  // per-kind float builds (RBP, CIRBP, ME-CIRBP; modes 2, 3)
 void* dyn_f32_minsum_get(int mode, int kind, int g16);
 void* dyn_trace_f64_exact_get(int mode);
 void* dyn_trace_f64_minsum_get(int mode);
@@ -32,6 +33,8 @@ inline void* ldpc_dyn_kernel(int f64, int kernel, int mode, int kind, int g16, i
     return kernel == KERNEL_EXACT ? dyn_trace_f32_exact_get(mode) : dyn_trace_f32_minsum_get(mode);
   }
   if (g16 && mode == 0) return nullptr;
+  if (!f64 && kernel == KERNEL_EXACT && !g16)
+    if (void* k = dyn_f32_exact_k_get(mode, kind)) return k;
   if (!f64) return kernel == KERNEL_EXACT ? dyn_f32_exact_get(mode, -1, g16) : dyn_f32_minsum_get(mode, -1, g16);
   if (kernel != KERNEL_EXACT) return dyn_f64_minsum_get(mode, -1, g16);
   switch (kind) {

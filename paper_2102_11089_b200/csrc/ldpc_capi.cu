@@ -218,10 +218,9 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
   p.slotE_bytes = align16(o);
   // N part
   o = 0;
-  p.o_total = take(N * sizeof(T));
-  p.o_pretot = take(ci || s->want_trace ? 2 * N * sizeof(T) : 0);  // (pre_total, p0(total)) pairs
+  // per-VN state: 4-word records (pre_total, p0(total), total, ci)
+  p.o_total = take(4 * N * sizeof(T));
   p.pt_on = s->want_trace && !ci ? 1 : 0;
-  p.o_ci = take(ci ? N * sizeof(T) : 0);
   p.o_inpp = take(s->kind == KIND_ME_LMD_CIRBP ? (N + 3) / 4 * 4 : 0);
   p.fast_sel = (me && s->kind != KIND_ME_RBP && s->n_g <= 255) ? 1 : 0;
   p.o_gid = take(p.fast_sel ? (N + 3) / 4 * 4 : 0);
@@ -253,7 +252,8 @@ void dyn_layout(const ldpc_graph* G, const ldpc_sched_t* s, DynParams& p) {
     return r;
   };
   const long long dl = std::max<long long>(G->max_items + 2, np + 1);
-  p.so_items = (int)stake(G->d.hop_items ? 0 : (long long)G->max_items * 16);  // items built on the fly
+  p.so_items = (int)stake(G->d.hop_items ? 0 : (long long)G->max_items * 8);  // items built on the fly
+  stake(kCounters * 8);  // the frame's work counters sit just below the stage area (Ctx::cntp)
   p.so_stage = (int)stake(std::max<long long>(((long long)G->max_items + 32) * sizeof(T), 32 * (4 + sizeof(Key))));
   p.so_nk = (int)stake((long long)G->max_items * std::max(sizeof(Key), sizeof(T)));  // keys; staged C2V values
   p.so_opre = (int)stake(ci || s->want_trace ? (long long)G->max_items * sizeof(T) : 0);
@@ -636,6 +636,9 @@ int validate(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if ((s->kind == KIND_ME_CIRBP || s->kind == KIND_ME_LMD_CIRBP) && s->n_p > G->d.N)
     return LDPC_ERR_INVALID;  // schedules.py:136-137
   if (is_dynamic(s->kind) && G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
+  // packed two-hop item records (dyn_engine.cuh Item): degree and stage offsets must fit
+  if (is_dynamic(s->kind) && (G->max_dc > kItemMaxDegree || G->max_items + G->max_dv > kItemMaxStage))
+    return LDPC_ERR_UNSUPPORTED;
   if (!is_dynamic(s->kind) && G->max_dc > kTileEdges) return LDPC_ERR_UNSUPPORTED;
   if (s->n_g > 4096) return LDPC_ERR_UNSUPPORTED;
   if (s->placement < 0 || s->placement > 4) return LDPC_ERR_INVALID;
@@ -765,7 +768,8 @@ __global__ void select_vns_kernel(const double* ci, const uint8_t* mask, int N, 
   memset(&c, 0, sizeof(c));
   c.w = Grp<32>::make();
   c.lane = c.w.lane;
-  c.ci = const_cast<double*>(ci);
+  c.nb = const_cast<double*>(ci) - 3;  // dense CI vector: ci(n) = nb[cs * n + 3]
+  c.cs = 1;
   c.sizes = (int*)smem;
   c.members = (int*)(smem + align16((long long)n_g * 4));
   uint8_t* excl = (uint8_t*)(smem + align16((long long)n_g * 4) + align16((long long)(N > n_p ? N : n_p) * 4));
@@ -797,7 +801,8 @@ int replay_check(const ldpc_graph* G, const ldpc_sched_t* s, long long B) {
   if (!G || !s || B < 0) return LDPC_ERR_INVALID;
   if (s->kernel != KERNEL_EXACT && s->kernel != KERNEL_MINSUM) return LDPC_ERR_INVALID;
   if (s->precision != LDPC_F64 && s->precision != LDPC_F32) return LDPC_ERR_INVALID;
-  if (G->max_dv > 32) return LDPC_ERR_UNSUPPORTED;
+  if (G->max_dv > 32 || G->max_dc > kItemMaxDegree || G->max_items + G->max_dv > kItemMaxStage)
+    return LDPC_ERR_UNSUPPORTED;
   return LDPC_OK;
 }
 }  // namespace
@@ -978,10 +983,10 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
     hop_ptr[e + 1] = hop_ptr[e] + hop_n[e];
     hop_sbptr[e + 1] = hop_sbptr[e] + (vn_ptr[edge_vn[e] + 1] - vn_ptr[edge_vn[e]]);
   }
-  const bool want_tab = hop_ptr[E] * 16 + (long long)hop_sbptr[E] * 4 <= (256ll << 20);
+  const bool want_tab = hop_ptr[E] * 8 + (long long)hop_sbptr[E] * 4 <= (256ll << 20);
   std::vector<int> hop_items, hop_sb;
   if (want_tab) {
-    hop_items.reserve(4 * hop_ptr[E]);
+    hop_items.reserve(2 * hop_ptr[E]);
     hop_sb.reserve(hop_sbptr[E]);
     for (int e = 0; e < E; ++e) {
       const int m_star = edge_cn[e], n_star = edge_vn[e];
@@ -994,7 +999,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
         }
         hop_sb.push_back(sb);
         for (int g2 = a; g2 < b; ++g2)
-          if (g2 != f) hop_items.insert(hop_items.end(), {g2, a, b - a, sb});
+          if (g2 != f) hop_items.insert(hop_items.end(), {g2, pack_item(g2 - a, b - a, sb)});
         sb += b - a;
       }
     }
@@ -1160,7 +1165,7 @@ int ldpc_graph_create(const int32_t* edge_cn, const int32_t* edge_vn, const int3
       return LDPC_ERR_CUDA;
     }
     G->hop_block = hb;
-    G->d.hop_items = (const int4*)(hb + o_items);
+    G->d.hop_items = (const int2*)(hb + o_items);
     G->d.hop_ptr = (const long long*)(hb + o_ptr);
     G->d.hop_sbptr = (const int*)(hb + o_sbp);
     G->d.hop_sb = (const int*)(hb + o_sb);

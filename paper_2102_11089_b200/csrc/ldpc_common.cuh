@@ -45,7 +45,7 @@ struct DevGraph {
   const uint8_t* hop_dup;   // [E]  1 if a VN repeats in that set (4-cycle through n*)
   // optional precomputed two-hop tables (null when they would be too large):
   const long long* hop_ptr; // [E]  offset of e's item records in hop_items
-  const int4* hop_items;    // item records (g, check start, check degree, stage base)
+  const int2* hop_items;    // item records (g, packed skip | degree | stage base: dyn_engine.cuh Item)
   const int* hop_sbptr;     // [E]  offset of e's per-VN-slot stage bases in hop_sb
   const int* hop_sb;        // stage base of each vn_edges slot of vn(e) (-1 for cn(e))
   // optional per-VN two-hop VN sets (sorted; null when too large): ME round pairing
@@ -405,7 +405,7 @@ struct Grp {
 // Rows of boundary k (E:204-207) -- and, once converged, of every later
 // boundary (E:215-217) -- plus their J(gamma) counts, D = |p0(total) -
 // p0(pre_total)| in float64 like the reference's post-processing of the trace.
-template <typename T, int G, int PS = 1>  // PS: stride of the pre_total column
+template <typename T, int G, int PS = 1>  // PS: word stride of the total and pre_total columns
 __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* total, const T* pretot, long long f,
                                     int k, bool conv, const Grp<G>& w) {
   if (!to.trace && !to.jc) return;
@@ -414,7 +414,7 @@ __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* t
     for (int kk = k; kk <= last; ++kk) {
       double* row = to.trace + (f * (I + 1) + kk) * 2ll * N;
       for (int n = w.lane; n < N; n += G) {
-        row[n] = (double)total[n];
+        row[n] = (double)total[PS * n];
         row[N + n] = (double)pretot[PS * n];
       }
     }
@@ -423,7 +423,7 @@ __device__ void trace_boundary_rows(const TraceOut& to, int N, int I, const T* t
       const double gm = to.gammas[gi];
       int ok = 0, bad = 0;
       for (int n = w.lane; n < N; n += G) {
-        const double t = (double)total[n];
+        const double t = (double)total[PS * n];
         const double d = fabs(p0(t) - p0((double)pretot[PS * n]));
         if (d >= gm) {
           if (t >= 0.0) ++ok;
