@@ -64,6 +64,9 @@ WORKLOADS = {
 }
 
 CI_KINDS = {"cirbp", "lmd_cirbp", "me_cirbp", "me_lmd_cirbp"}
+# random 32-byte-sector read bandwidth of HBM at a >= 4 GB footprint, measured on the pool's
+# B200s with tools/micro/randbw (profiles/r2/r2m_random_sector_bandwidth.json)
+RANDOM_SECTOR_GBPS = 1170.0
 
 
 def bytes_per_update(kind, counters, E, N, elem):
@@ -462,10 +465,20 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
         "roofline": {"bound": "hbm", "kernel": list(per)[dom], "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
+                     # the dynamic schedules touch scattered 32-byte sectors of a multi-GB state:
+                     # the HBM figure that bounds them is the random-sector rate measured by
+                     # tools/micro/randbw (profiles/r2/r2m_random_sector_bandwidth.json), not the copy rate
+                     "random_sector_peak": RANDOM_SECTOR_GBPS,
+                     "dram_rate": (traffic / (sched_ms[dom] / 1e3) / 1e9) if traffic else None,
+                     "dram_rate_vs_random_sector_peak":
+                         (traffic / (sched_ms[dom] / 1e3) / 1e9 / RANDOM_SECTOR_GBPS) if traffic else None,
                      "note": "achieved = algorithmic message-state bytes per launch (SURVEY 8(d) "
                              "formula in %s units x the launch's C2V updates) / the launch's CUDA-event "
-                             "time; the dynamic schedules are a serial update chain per frame "
-                             "(latency-bound), so this fraction is low by construction" % args.precision},
+                             "time; peak = HBM copy bandwidth.  The dynamic schedules read and write "
+                             "scattered sectors (8 useful bytes per 32-byte sector for the per-VN words), "
+                             "so their DRAM traffic (`traffic`, ncu) is 3-5x the algorithmic bytes and the "
+                             "bound that applies is the random-sector rate (`random_sector_peak`, GB/s "
+                             "of 32-byte sectors at >= 4 GB footprint)" % args.precision},
         "e2e": {"value": e2e_value, "unit": "C2V edge updates/s", "h2d_bytes_per_step": h2d // steps,
                 "d2h_bytes_per_step": d2h // steps} if e2e else None,
         "gpu_launches": launches,
