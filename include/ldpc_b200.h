@@ -33,7 +33,8 @@ extern "C" {
 /* error codes */
 #define LDPC_OK 0
 #define LDPC_ERR_INVALID (-1)     /* bad argument (mirrors the reference's ValueError) */
-#define LDPC_ERR_UNSUPPORTED (-2) /* graph exceeds a kernel limit (d_v > 32 or d_c > 32) */
+#define LDPC_ERR_UNSUPPORTED (-2) /* graph exceeds a kernel limit: dynamic schedules d_v <= 32, d_c <= 255 and \
+                                     a two-hop set (+ d_v) below 65536; fixed schedules d_c <= one tile */
 #define LDPC_ERR_CUDA (-3)        /* CUDA runtime error */
 #define LDPC_ERR_WORKSPACE (-4)   /* workspace smaller than ldpc_workspace_size() */
 

@@ -183,10 +183,39 @@ struct Ctx {
   int it;            // completed iterations
   int lane;          // lane within the group (= w.lane)
   long long rng;
+  // Every lane of a whole-warp group performs the same read-add-write (same
+  // address, same value: one of the identical stores lands), so there is no
+  // divergent lane-0 branch; the half-warps of a pair step add atomically.
   __device__ __forceinline__ void count(int k, long long v) {
-    if (lane == 0) {
-      if (G == 32) cntp()[k] += v;
-      else atomicAdd((unsigned long long*)&cntp()[k], (unsigned long long)v);  // half-warps of a pair step share them
+    if constexpr (G == 32) {
+      cntp()[k] += v;
+    } else {
+      if (lane == 0) atomicAdd((unsigned long long*)&cntp()[k], (unsigned long long)v);
+    }
+  }
+  // one update's V2C and pre-C2V tallies (adjacent counters 1 and 2).  C_PROP
+  // (= prop) and C_CI (= C_PRE for CI kinds) are filled in when the frame ends.
+  __device__ __forceinline__ void count_update(int v2c, int pre) {
+    static_assert(C_V2C == 1 && C_PRE == 2, "adjacent counters");
+    if constexpr (G == 32) {
+      long long* q = cntp() + C_V2C;
+      q[0] += v2c;
+      q[1] += pre;
+    } else {
+      if (lane == 0) {
+        atomicAdd((unsigned long long*)&cntp()[C_V2C], (unsigned long long)v2c);
+        atomicAdd((unsigned long long*)&cntp()[C_PRE], (unsigned long long)pre);
+      }
+    }
+  }
+  // frame end: counters[f][0..8) with the derived ones (group-converged; syncs first)
+  __device__ __forceinline__ void store_counters(long long* out, bool ci_kind) const {
+    w.sync();
+    if (lane < kCounters) {
+      long long v = cntp()[lane];
+      if (lane == C_PROP) v = prop;
+      if (lane == C_CI) v = ci_kind ? cntp()[C_PRE] : 0;
+      out[lane] = v;
     }
   }
 };
@@ -625,6 +654,19 @@ __device__ __forceinline__ void note_ci_group(Ctx<T, G>& c, int n_g, int W, int 
   }
 }
 
+// CIRBP's CI tree is built over THRESHOLDED keys: a CI below gamma counts as 0.
+// CIRBP only asks for the max-CI VN n* and whether ci[n*] < gamma (E:409-417):
+// if some CI >= gamma the thresholded maximum is the true one (same lowest-index
+// tie-break); if none is, the tree returns VN 0, whose CI is < gamma like the
+// true maximum's, and both take the residual-argmax branch -- identical
+// decisions and counters.  The gain: a refreshed VN whose CI was and stays below
+// gamma (the vast majority of the ~90 per BG1 update, gamma = 0.1) does not
+// touch the tree at all.
+template <typename T>
+__device__ __forceinline__ typename Num<T>::Key ci_tree_key(T ci, T gamma) {
+  return Num<T>::key(ci >= gamma ? ci : T(0));
+}
+
 // ------------------------------------------------------------- propagate
 
 // E:130-176.  Commit pre_c2v[e*], emit V2C to M(n*)\m*, refresh the two-hop
@@ -664,14 +706,15 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   if (lane < vr.y) adj = g.vadj[vr.x + lane];
   const bool act = lane < vr.y && adj.y != m_star;
   int sb0 = 0;  // stage base of this lane's check (loaded with the records above, not after the commit)
-  if (tab && lane < vr.y) sb0 = g.hop_sb[hsp + lane];
+  if (PF && tab && lane < vr.y) sb0 = g.hop_sb[hsp + lane];
   const T old = c.c2v[e_star];
   const T nv = c.pre[e_star];
   const T tot = c.total(n_star) + (nv - old);  // E:147
   T ptn = T(0);  // pre_total of n* (unchanged by this update: the items exclude n*'s edges)
   T cin = T(0);  // CI of n* before this update (its Alg.-4 group)
   if (CI) ptn = c.pretot(n_star);
-  if (CI && MG) cin = c.ci(n_star);
+  if (CI && (MG || CT)) cin = c.ci(n_star);
+  const T gam = (T)p.gamma;  // CT: threshold of the CI-tree keys
   const T cf = act ? c.c2v[adj.x] : T(0);
   if (pf) {
     // stage the two-hop inputs now: they do not depend on this update's V2C
@@ -744,8 +787,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     int sbase = 0;
     if (tab) {
-      sbase = sb0;
-      if (k0 > 0 && k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
+      if (PF && k0 == 0) sbase = sb0;
+      else if (k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
     } else {
       n_items = build_items_from<T, G>(c, a2, act2, &sbase, ci_, cs_);
     }
@@ -818,7 +861,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       if (!dup) {
         if (valid) {
           const typename Vec2<T>::type pq = *reinterpret_cast<const typename Vec2<T>::type*>(c.nb + 4 * j);
-          if (CI && MG) oci = c.ci(j);  // same sector as pq
+          if (CI && (MG || CT)) oci = c.ci(j);  // same sector as pq
           x = pq.x + delta;  // E:171
           c.pretot(j) = x;
           if (CI) {
@@ -840,7 +883,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (CI && last) {
           x = c.pretot(j);
           cache = c.p0t(j);
-          if (MG) oci = c.ci(j);
+          if (MG || CT) oci = c.ci(j);
           want = true;
         }
         if (CT && valid) c.cj[t] = last ? j : -1;  // only the VN's final CI enters the tree
@@ -857,7 +900,11 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (want) {
           const T cv = CiSplit<T>::join(cache, pr);
           c.ci(j) = cv;
-          if (CT) c.ck[t] = Num<T>::key(cv);
+          if (CT) {
+            const Key kk = ci_tree_key<T>(cv, gam);
+            c.ck[t] = kk;
+            if (kk == ci_tree_key<T>(oci, gam) && !(cv >= gam)) c.cj[t] = -1;  // below gamma before and after
+          }
           if (MG && p.fast_sel) note_ci_group(c, p.n_g, (p.g.N + 31) >> 5, j, cv, oci);
         } else if (self && t == ps0) {
           const T cv = kSelf == 2 ? Num<T>::abs_(pr - pr_next) : pr;
@@ -1035,8 +1082,10 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int* se = (int*)c.stage;  // stage is free again: G (index, key) pairs
     Key* sk = (Key*)(se + 32);
     int nrec = 0, ndirty = 0;
-    apply_leaf_updates(c.ct, geo, lane == 0 ? n_star : -1, Num<T>::key(c.ci(n_star)), w, se, sk, c.dl1, nrec,
-                       c.dl0, ndirty);
+    const T cnew = c.ci(n_star);
+    if (cnew >= gam || cin >= gam)
+      apply_leaf_updates(c.ct, geo, lane == 0 ? n_star : -1, ci_tree_key<T>(cnew, gam), w, se, sk, c.dl1, nrec,
+                         c.dl0, ndirty);
     for (int base = 0; base < n_items; base += G) {  // (VN, key) pairs staged by the refresh
       const int t = base + lane;
       int j = -1;
@@ -1045,18 +1094,16 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         j = c.cj[t];
         kk = j >= 0 ? c.ck[t] : Key(0);
       }
+      if (!w.any(j >= 0)) continue;  // every VN of this pass stayed below gamma
       apply_leaf_updates(c.ct, geo, j, kk, w, se, sk, c.dl1, nrec, c.dl0, ndirty);
     }
-    auto cleaf = [&](int n) -> Key { return Num<T>::key(c.ci(n)); };
+    auto cleaf = [&](int n) -> Key { return ci_tree_key<T>(c.ci(n), gam); };
     group_recompute_list(c.ct, geo, c.dl1, nrec, w, cleaf);
     w.sync();
     l2_finish(c.ct, geo, c.dl1, nrec, c.dl0, ndirty, c.dl0 + (geo.levels > 2 ? p.dl_cap : 0), w, cleaf);
   }
   if (MG && p.fast_sel) w.sync();
-  c.count(C_PROP, 1);
-  c.count(C_V2C, vr.y - 1);
-  c.count(C_PRE, n_items);
-  if (CI) c.count(C_CI, n_items);
+  c.count_update(vr.y - 1, n_items);
   return n_items;
 }
 
@@ -1716,13 +1763,14 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
       }
     } break;
     case KIND_CIRBP: {  // E:388-433
-      tree_build(c.rt, p.rgeo, c.w, rleaf);
-      tree_build(c.ct, p.cgeo, c.w, cleaf);
       const T gamma = (T)p.gamma;
+      auto tleaf = [&](int n) -> Key { return ci_tree_key<T>(c.ci(n), gamma); };  // thresholded CI-tree keys
+      tree_build(c.rt, p.rgeo, c.w, rleaf);
+      tree_build(c.ct, p.cgeo, c.w, tleaf);
       int kh = 0, kt = 0;  // per-iteration kappa tallies (warp-uniform)
       while (c.prop < budget) {
         const int it = c.it;
-        int n_star = tree_argmax(c.ct, p.cgeo, c.w, cleaf);
+        int n_star = tree_argmax(c.ct, p.cgeo, c.w, tleaf);
         c.count(C_CMP, g.N - 1 + 1);
         c.count(C_KTRIALS, 1);
         ++kt;
@@ -1913,8 +1961,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
   }
   if (I == 0) conv = syndrome_ok<T, G>(g, c.tb(), c.ts, c.w);  // schedules.py:144-146
   for (int n = lane; n < g.N; n += G) p.u_hat[f * g.N + n] = c.total(n) < T(0) ? 1 : 0;
-  c.w.sync();
-  if (lane < kCounters) p.counters[f * kCounters + lane] = c.cntp()[lane];
+  c.store_counters(p.counters + f * kCounters, ci_kind);
   if (lane == 0) {
     p.prop[f] = c.prop;
     p.conv[f] = conv ? 1 : 0;
@@ -2066,8 +2113,7 @@ __global__ void __launch_bounds__(32) dyn_replay_kernel(const __grid_constant__ 
     o[2 * g.E + g.N + n] = (double)c.pretot(n);
     o[2 * g.E + 2 * g.N + n] = (double)c.ci(n);
   }
-  c.w.sync();
-  if (c.lane < kCounters) p.counters[f * kCounters + c.lane] = c.cntp()[c.lane];
+  c.store_counters(p.counters + f * kCounters, true);
 }
 
 }  // namespace ldpc

@@ -330,16 +330,19 @@ struct Grp {
   int base_;       // first warp lane of the group
   int lane;        // lane within the group
   unsigned lt;     // group-local mask of lower lanes
-  // a whole warp (G = 32): compile-time constants, so shuffles / votes / syncs
-  // take the immediate full-mask forms
-  __device__ __forceinline__ unsigned mask() const { return G == 32 ? kFull : mask_; }
+  // The mask stays a run-time value even for a whole warp (G = 32, loaded through
+  // an opaque move in make()): with an immediate full mask nvcc guards every
+  // shuffle / vote / reduction with a convergence check and a WARPSYNC.COLLECTIVE
+  // slow path (37 of them in the LMDRBP kernel, +25 % executed instructions).
+  __device__ __forceinline__ unsigned mask() const { return mask_; }
   __device__ __forceinline__ int base() const { return G == 32 ? 0 : base_; }
   __device__ __forceinline__ static Grp make() {
     Grp g;
     const int wl = threadIdx.x & 31;
     g.base_ = G == 32 ? 0 : (wl / G) * G;
     g.lane = wl - g.base_;
-    g.mask_ = G == 32 ? kFull : (((1u << G) - 1u) << g.base_);
+    if (G == 32) asm("mov.b32 %0, 0xffffffff;" : "=r"(g.mask_));
+    else g.mask_ = ((1u << G) - 1u) << g.base_;
     g.lt = (1u << g.lane) - 1u;
     return g;
   }
