@@ -329,6 +329,14 @@ def run_ours(args, wl):
         # clock: one step is minutes of GPU time, so 1 warm-up + 1 timed step
         sec = measure(args, WORKLOADS["C3"], "C3", 1, 1, rank, world, local, batch=0, cpu=cpu, e2e=False)
         line["secondary"] = {"C3": {k: sec[k] for k in sec if k not in ("e2e",)}}
+        if args.secondary_f32:
+            # the same C3 block with float32 state (the north star's GPU arithmetic: half the
+            # sectors per update; parity there is 1e-4 on message values, not bit identity)
+            import copy
+            a32 = copy.copy(args)
+            a32.precision = "f32"
+            s32 = measure(a32, WORKLOADS["C3"], "C3", 1, 1, rank, world, local, batch=0, cpu=False, e2e=False)
+            line["secondary"]["C3_f32"] = {k: s32[k] for k in s32 if k not in ("e2e",)}
     if rank == 0:
         print(json.dumps(line, default=_json_default), flush=True)
     if world > 1:
@@ -526,6 +534,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C3 block of the default C1 run")
+    ap.add_argument("--secondary-f32", action="store_true", help="also run the C3 block with float32 state")
     ap.add_argument("--only", default="", help="run one schedule of the workload (e.g. cirbp, me_rbp/M4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT"):
