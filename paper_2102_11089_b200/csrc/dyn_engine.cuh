@@ -567,15 +567,16 @@ __device__ int argmax_scan(int n, const Grp<G>& w, KeyFn keyf) {
 }
 
 // E:269-276 -- first maximum residual over M(n) in vn_edges order (= edge order)
-template <typename T, int G>
+template <typename T, int G, bool KEEP = false>  // KEEP: L2 evict_last hint on the graph tables (ldk)
 __device__ __forceinline__ int argmax_vn_edges(const DevGraph& g, const Ctx<T, G>& c, int n, int* deg = nullptr) {
   using Key = typename Num<T>::Key;
-  const int2 vr = g.vrec[n];
+  const unsigned long long pol = KEEP ? l2_keep_policy() : 0ull;
+  const int2 vr = ldk<KEEP>(g.vrec + n, pol);
   if (deg) *deg = vr.y;  // the caller's comparison count, without reloading vrec
   Key bk = 0;
   int be = 0x7fffffff;
   for (int k = c.lane; k < vr.y; k += G) {  // vn_edges ascend: first max = lowest edge
-    const int e = g.vn_edges[vr.x + k];
+    const int e = ldk<KEEP>(g.vn_edges + vr.x + k, pol);
     const Key kk = res_key<T, false, G>(c, e);
     if (kk > bk || be == 0x7fffffff) { bk = kk; be = e; }
   }
@@ -691,22 +692,24 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
   // the V2C inputs and ALL two-hop inputs / C2V values / pre values together.
   const bool tab = g.hop_items != nullptr;
   const bool pf = PF && tab;
+  // graph-table loads keep their lines in L2 where the state streams from HBM (ldk)
+  const unsigned long long pol = PF ? l2_keep_policy() : 0ull;
   int n_items = 0, hsp = 0;
   if (tab) {
-    c.items = g.hop_items + g.hop_ptr[e_star];
-    n_items = g.hop_n[e_star];
-    hsp = g.hop_sbptr[e_star];
+    c.items = g.hop_items + ldk<PF>(g.hop_ptr + e_star, pol);
+    n_items = ldk<PF>(g.hop_n + e_star, pol);
+    hsp = ldk<PF>(g.hop_sbptr + e_star, pol);
   } else {
     c.items = c.items_buf;
   }
-  const int4 er = g.erec[e_star];  // (m*, n*, vn_ptr[n*], d_v(n*))
+  const int4 er = ldk<PF>(g.erec + e_star, pol);  // (m*, n*, vn_ptr[n*], d_v(n*))
   const int m_star = er.x, n_star = er.y;
   const int2 vr = make_int2(er.z, er.w);
   int4 adj = make_int4(-1, -1, 0, 0);
-  if (lane < vr.y) adj = g.vadj[vr.x + lane];
+  if (lane < vr.y) adj = ldk<PF>(g.vadj + vr.x + lane, pol);
   const bool act = lane < vr.y && adj.y != m_star;
   int sb0 = 0;  // stage base of this lane's check (loaded with the records above, not after the commit)
-  if (PF && tab && lane < vr.y) sb0 = g.hop_sb[hsp + lane];
+  if (PF && tab && lane < vr.y) sb0 = ldk<PF>(g.hop_sb + hsp + lane, pol);
   const T old = c.c2v[e_star];
   const T nv = c.pre[e_star];
   const T tot = c.total(n_star) + (nv - old);  // E:147
@@ -722,9 +725,9 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     // with pre_total upkeep, its old pre) for the refresh; two items per pass
     for (int t = lane; t < n_items; t += 2 * G) {
       const int t2 = t + G;
-      const Item r = unpack_item(c.items[t]);
+      const Item r = unpack_item(ldk<PF>(c.items + t, pol));
       Item r2 = r;
-      if (t2 < n_items) r2 = unpack_item(c.items[t2]);
+      if (t2 < n_items) r2 = unpack_item(ldk<PF>(c.items + t2, pol));
       const T x = c.in[r.g], cg = c.c2v[r.g];
       const T x2 = c.in[r2.g], cg2 = c.c2v[r2.g];
       T op = T(0), op2 = T(0);
@@ -732,8 +735,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
       if (PT) {
         op = c.pre[r.g];
         op2 = c.pre[r2.g];
-        j1 = g.edge_vn[r.g];
-        j2 = g.edge_vn[r2.g];
+        j1 = ldk<PF>(g.edge_vn + r.g, pol);
+        j2 = ldk<PF>(g.edge_vn + r2.g, pol);
       }
       c.stage[r.sb + r.skip] = x;
       c.cg[t] = cg;
@@ -781,14 +784,14 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     if (k0 > 0) {
       const int k = k0 + lane;
       a2 = make_int4(-1, -1, 0, 0);
-      if (k < vr.y) a2 = g.vadj[vr.x + k];
+      if (k < vr.y) a2 = ldk<PF>(g.vadj + vr.x + k, pol);
       act2 = k < vr.y && a2.y != m_star;
       cf2 = act2 ? c.c2v[a2.x] : T(0);
     }
     int sbase = 0;
     if (tab) {
       if (PF && k0 == 0) sbase = sb0;
-      else if (k0 + lane < vr.y) sbase = g.hop_sb[hsp + k0 + lane];
+      else if (k0 + lane < vr.y) sbase = ldk<PF>(g.hop_sb + hsp + k0 + lane, pol);
     } else {
       n_items = build_items_from<T, G>(c, a2, act2, &sbase, ci_, cs_);
     }
@@ -807,7 +810,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     }
     w.sync();
   }
-  const bool dup = PT && g.hop_dup[e_star] != 0;
+  const bool dup = PT && ldk<PF>(g.hop_dup + e_star, pol) != 0;
+  auto item_g = [&](int t) -> int { return ldk<PF>((const int*)(c.items + t), pol); };  // edge id of item t
   // n*'s own CI (E:148-149: its total changed, its pre_total did not) rides on
   // spare lanes of the refresh -- kSelf pseudo-items right after the real ones
   // (kept inside one pass) -- so no lane evaluates an exp/division chain alone.
@@ -823,7 +827,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     int j = -1;
     T delta = T(0);
     if (valid) {
-      const Item r = unpack_item(c.items[t]);
+      const Item r = unpack_item(ldk<PF>(c.items + t, pol));
       const int ge = r.g, skip = r.skip;
       // independent loads first (the pre[] store below would otherwise pin them)
       const T cg = pf ? c.cg[t] : c.c2v[ge];
@@ -934,8 +938,8 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
     for (int base = 0; base < n_items; base += G) {
       const int t = base + lane;
       const bool valid = t < n_items;
-      const int q = valid ? (c.items[t].x >> 5) : -1;
-      const int qp = (valid && t > 0) ? (c.items[t - 1].x >> 5) : -2;
+      const int q = valid ? (item_g(t) >> 5) : -1;
+      const int qp = (valid && t > 0) ? (item_g(t - 1) >> 5) : -2;
       const bool start = valid && q != qp;
       const unsigned bal = w.ballot(start);
       if (start) segs[nseg + __popc(bal & w.lt)] = t;
@@ -955,7 +959,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
         if (si < nseg) {
           a = segs[si];
           b = segs[si + 1];
-          q = c.items[a].x >> 5;
+          q = item_g(a) >> 5;
         } else {
           q = qs;
         }
@@ -973,7 +977,7 @@ __device__ int propagate(const DynParams& p, Ctx<T, G>& c, int e_star) {
           if (e_star == I) { hasI = true; nI = k0; }
         }
         for (int t = a; t < b; ++t) {
-          const int e = c.items[t].x;
+          const int e = item_g(t);
           const Key kk = c.nk[t];
           if (kk > mx || (kk == mx && e < mi)) { mx = kk; mi = e; }
           if (e == I) { hasI = true; nI = kk; }
@@ -1782,7 +1786,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
           e = tree_argmax(c.rt, p.rgeo, c.w, rleaf);
           c.count(C_CMP, E - 1);
         } else {
-          e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
+          e = argmax_vn_edges<T, G, PF>(g, c, n_star, &dv_);
           c.count(C_CMP, dv_ - 1);
         }
         propagate<T, KERNEL, true, true, true, false, G, false, TR, PF>(p, c, e);
@@ -1818,7 +1822,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
     case KIND_LMD_CIRBP: {  // E:555-598
       int n_star = argmax_scan<Key>(g.N, c.w, cleaf);
       c.count(C_CMP, g.N - 1);
-      int e = argmax_vn_edges<T, G>(g, c, n_star, &dv_);
+      int e = argmax_vn_edges<T, G, PF>(g, c, n_star, &dv_);
       c.count(C_CMP, dv_ - 1);
       while (c.prop < budget) {
         int n_items = propagate<T, KERNEL, true, false, false, false, G, false, TR, PF>(p, c, e);
@@ -1848,7 +1852,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
             }
           }
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
+          int e = argmax_vn_edges<T, G, PF>(g, c, pv, &dv_);
           c.count(C_CMP, dv_ - 1);
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);
           ++c.prop;
@@ -1871,7 +1875,7 @@ __device__ void decode_frame(const DynParams& p, Ctx<T, G>& c, long long f) {
             }
           }
           int pv = c.sel[idx];
-          int e = argmax_vn_edges<T, G>(g, c, pv, &dv_);
+          int e = argmax_vn_edges<T, G, PF>(g, c, pv, &dv_);
           c.count(C_CMP, dv_ - 1);
           if (lane == 0) c.chosen[idx] = e;
           propagate<T, KERNEL, true, false, false, false, G, true, TR, PF>(p, c, e);

@@ -260,6 +260,49 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Loads of the immutable graph tables with an L2 evict_last hint (KEEP = the
+// HBM placement of a BG-sized code).  There ~1.7 TB/s of per-frame state streams
+// through the 126 MB L2, so a line survives ~70 us while a given table line is
+// re-read only every few hundred us: without the hint the ~95 MB of tables
+// (two-hop items, edge / VN records) are read from HBM on every update, ~20 %
+// of its DRAM requests.
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <bool KEEP> __device__ __forceinline__ int ldk(const int* p, unsigned long long pol) {
+  if (!KEEP) return *p;
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <bool KEEP> __device__ __forceinline__ int ldk(const uint8_t* p, unsigned long long pol) {
+  if (!KEEP) return *p;
+  int v;
+  asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <bool KEEP> __device__ __forceinline__ long long ldk(const long long* p, unsigned long long pol) {
+  if (!KEEP) return *p;
+  long long v;
+  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <bool KEEP> __device__ __forceinline__ int2 ldk(const int2* p, unsigned long long pol) {
+  if (!KEEP) return *p;
+  int2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+template <bool KEEP> __device__ __forceinline__ int4 ldk(const int4* p, unsigned long long pol) {
+  if (!KEEP) return *p;
+  int4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Warp max of keys (REDUX) -> lowest lane holding it.  Returns (key, lane).
 __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k, int* lane_out) {
   unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
