@@ -1334,11 +1334,22 @@ __device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl,
         if (bal) hit = c.w.shfl(h ? ov[2 * (i0 + lane) + 1] : 0, 31 - __clz(bal));
       }
       if (hit >= 0) return hit;
+      // the bitmap word holding member `pos`: the last word with wpre <= pos
+      // (wpre is non-decreasing, wpre[0] = 0).  Two votes -- every S-th word,
+      // then the S words of that block -- instead of a linear scan (BG1: 816 words)
       int nle = 0;
-      for (int base = 0; base < W; base += G) {
-        const unsigned bal = c.w.ballot(base + lane < W && wpre[base + lane] <= pos);
-        nle += __popc(bal);
-        if (bal != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
+      const int S = (W + G - 1) / G;
+      if (S <= G) {
+        const unsigned b1 = c.w.ballot(lane * S < W && wpre[lane * S] <= pos);
+        const int b0 = (__popc(b1) - 1) * S;
+        const unsigned b2 = c.w.ballot(lane < S && b0 + lane < W && wpre[b0 + lane] <= pos);
+        nle = b0 + __popc(b2);
+      } else {
+        for (int base = 0; base < W; base += G) {
+          const unsigned bal = c.w.ballot(base + lane < W && wpre[base + lane] <= pos);
+          nle += __popc(bal);
+          if (bal != (G == 32 ? 0xffffffffu : (1u << G) - 1u)) break;
+        }
       }
       const int wsel = nle - 1;
       return wsel * 32 + (int)__fns(fb[wsel], 0, pos - wpre[wsel] + 1);
