@@ -450,8 +450,14 @@ def measure(args, wl, wname, steps, warmup, rank, world, local, batch=0, cpu=Fal
     tf = ROOT / "profiles" / "traffic.json"
     dom_name = cfgs[dom].kind + (f"/M{cfgs[dom].n_p}" if cfgs[dom].kind.startswith("me_") else "")
     if tf.exists():
-        t = json.loads(tf.read_text()).get(f"{key}:{dom_name}:{args.precision}:{batch}")
+        tj = json.loads(tf.read_text())
+        t = tj.get(f"{key}:{dom_name}:{args.precision}:{batch}")
         traffic = t.get("dram_bytes_per_launch") if t else None
+        if traffic is None:
+            # no capture of this exact launch: a per-update figure measured on the same code,
+            # schedule and placement at full occupancy (ncu dram bytes / updates) x this launch's updates
+            t = tj.get(f"{key}:{dom_name}:{args.precision}:per_update")
+            traffic = t["dram_bytes_per_update"] * work[dom]["updates"] if t else None
     per = {}
     for i, (c, wk) in enumerate(zip(cfgs, work)):
         nm = c.kind + (f"/M{c.n_p}" if c.kind.startswith("me_") else "")

@@ -1339,7 +1339,7 @@ __device__ int select_vns(const DynParams& p, Ctx<T, G>& c, const uint8_t* excl,
       // then the S words of that block -- instead of a linear scan (BG1: 816 words)
       int nle = 0;
       const int S = (W + G - 1) / G;
-      if (S <= G) {
+      if (S <= G && W > G) {
         const unsigned b1 = c.w.ballot(lane * S < W && wpre[lane * S] <= pos);
         const int b0 = (__popc(b1) - 1) * S;
         const unsigned b2 = c.w.ballot(lane < S && b0 + lane < W && wpre[b0 + lane] <= pos);

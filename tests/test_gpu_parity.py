@@ -102,6 +102,24 @@ def test_c0_batch_vs_oracle(kind):
     _compare_oracle(spec, g, llrs, _cfg({"kind": kind, "i_max": 5, "n_p": 4}))
 
 
+@pytest.mark.parametrize("code_key,eb,count", [("C0", 2.0, 600), ("C1", 1.5, 400), ("C2", 1.0, 96)])
+@pytest.mark.parametrize("gamma", [0.0, 1e-6, 0.3, 0.9, 0.999999])
+def test_cirbp_gamma_sweep_vs_oracle(code_key, eb, count, gamma):
+    """CIRBP's CI tree holds keys thresholded at gamma (dyn_engine.cuh ci_tree_key):
+    decisions, update counts, all counters (incl. the kappa hits / trials of
+    E:411-415) must equal the oracle's for any gamma -- 0 (no thresholding), tiny,
+    typical, and so large that every selection falls back to the residual argmax."""
+    spec, g = load_code(code_key)
+    llrs = llr_batch(spec, eb, seed=3, start=0, count=count)
+    cfg = _cfg({"kind": "cirbp", "i_max": 3, "gamma": gamma})
+    _compare_oracle(spec, g, llrs, cfg)
+    got = _gpu(spec, llrs, cfg)
+    ref = pyoracle.decode_batch(g, llrs.astype(np.float64), "cirbp", cfg.kernel, cfg.i_max, spec.k_info, gamma,
+                                cfg.n_p, cfg.n_g, cfg.selection_seed)
+    same = (got["u_hat"] == ref["u_hat"]).all(1) & (got["prop"] == ref["prop"])
+    assert (got["counters"][same][:, 6:8] == ref["counters"][same][:, 6:8]).all()  # C_KHITS, C_KTRIALS
+
+
 @pytest.mark.parametrize("kind", ["layered", "rbp", "cirbp", "lmdrbp", "slmdrbp", "lmd_cirbp", "me_cirbp",
                                   "me_lmd_cirbp", "me_rbp"])
 def test_c1_batch_vs_oracle(kind):
