@@ -8,6 +8,7 @@ PART selects a slice of the grid (so each gpurun call stays bounded):
   c2      configs[2]: C2 at 0.5..2.0 dB, 100k frames, layered/RBP/CIRBP/ME-CIRBP M=1,4,16
   c3      configs[3]: C3 at 0.5 and 1.0 dB, 10k frames, flooding/layered/RBP/CIRBP/ME-CIRBP M=64
   c4      configs[4]: C2 code at 0 dB, i_max 20, batches 1..16k (all five schedules), 256k (two)
+  c4m     configs[4]: the 1M-frame batch, ME-CIRBP(64)
 
 One JSON line per (config, SNR, schedule, batch): GPU time (CUDA events, one
 untimed warm-up decode of up to 8192 frames first), frames/s, C2V updates/s, FER and info-BER over
@@ -47,6 +48,7 @@ PARTS = {
     "c3": [("C3", eb, 10, 10_000, C3S, 32) for eb in (0.5, 1.0)],
     "c4": [("C4", 0.0, 20, b, C4S, 0) for b in (1, 64, 1024, 16384)] +
           [("C4", 0.0, 20, 262_144, [("me_cirbp", 64), ("rbp", 1)], 0)],
+    "c4m": [("C4", 0.0, 20, 1_048_576, [("me_cirbp", 64)], 0)],  # the 1M-frame point (about 15 GPU-minutes)
 }
 
 
