@@ -49,6 +49,7 @@ PARTS = {
     "c4": [("C4", 0.0, 20, b, C4S, 0) for b in (1, 64, 1024, 16384)] +
           [("C4", 0.0, 20, 262_144, [("me_cirbp", 64), ("rbp", 1)], 0)],
     "c4m": [("C4", 0.0, 20, 1_048_576, [("me_cirbp", 64)], 0)],  # the 1M-frame point (about 15 GPU-minutes)
+    "c4r": [("C4", 0.0, 20, 1_048_576, [("rbp", 1)], 0)],
 }
 
 
